@@ -1,0 +1,173 @@
+/* pw_b200.h -- C ABI of the B200-native batched graph-ANNS search path.
+ *
+ * Drop-in boundary for the reference package shardann 0.1.0 (PathWeaver,
+ * arXiv 2507.17094).  The reference has no FFI of its own (pure Python +
+ * numpy); each entry point below replaces one reference interface, cited as
+ * /root/reference/pkg/src/shardann/<file>:<line>.  Plain pointers and sizes
+ * only; no torch or C++ types cross this boundary; no C++ exceptions escape.
+ *
+ * Status codes: 0 ok; PW_EINVAL (-1) -> ValueError, PW_ENOMEM (-2) ->
+ * MemoryError, PW_ECUDA (-3) -> RuntimeError.  pw_last_error() returns the
+ * thread-local message of the last failure (text matches the reference's
+ * ValueError messages where one exists).
+ */
+#ifndef PW_B200_H
+#define PW_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PW_OK 0
+#define PW_EINVAL (-1)
+#define PW_ENOMEM (-2)
+#define PW_ECUDA (-3)
+
+#define PW_DTYPE_F32 0
+#define PW_DTYPE_U8 1
+
+#define PW_SEL_FULL 0
+#define PW_SEL_DIRECTION 1
+#define PW_SEL_RANDOM 2
+
+#define PW_SEED_NEIGHBORS 0
+#define PW_SEED_MIXED 1
+
+#define PW_MODE_BASELINE 0
+#define PW_MODE_PIPELINED 1
+
+/* search.py:39-73 SearchParams (field for field). */
+typedef struct {
+    int32_t k, l, m, r, max_iter;
+    uint64_t seed;
+    int32_t selection;       /* PW_SEL_* */
+    double discard_ratio;
+    double cooldown_ratio;
+    int32_t ghost_enabled;
+    int32_t ghost_max_iter;
+    int32_t seed_mode;       /* PW_SEED_* */
+    int32_t buffer_cap;      /* 0 = None */
+    int32_t log_visits;
+} pw_params;
+
+/* Device-side knobs outside SearchParams (SURVEY.md §5 "Config"). 0 = default. */
+typedef struct {
+    int32_t visited_slots;   /* shared-memory visited-hash slots per query (power of 2) */
+    int32_t stage_rows;      /* rows in flight per warp (gather staging) */
+    int32_t warps_per_sm;    /* cap on resident query-warps per SM */
+} pw_tuning;
+
+/* One shard (pipeline.py:121-155 build_contexts output for one ShardPack):
+ * host arrays, copied to the current device by pw_shard_create. */
+typedef struct {
+    int64_t n;                    /* n_local */
+    int32_t d;
+    int32_t j;                    /* graph degree (adj.shape[1]); may be 0 */
+    int32_t dtype;                /* PW_DTYPE_* of vectors */
+    const void* vectors;          /* (n, d) row-major */
+    const int32_t* adj;           /* (n, j) shard-local ids */
+    const int32_t* global_ids;    /* (n,) */
+    const uint32_t* direction;    /* (n, j, ceil(d/32)) packed sign bits or NULL */
+    const int32_t* inter_map;     /* (n,) local ids in the next shard, or NULL */
+    int64_t ghost_n;              /* 0 = no ghost index */
+    int32_t ghost_j;
+    const int32_t* ghost_ids;     /* (ghost_n,) parent-local ids, sorted */
+    const int32_t* ghost_adj;     /* (ghost_n, ghost_j) ghost-local ids */
+} pw_shard_desc;
+
+typedef struct pw_shard pw_shard;
+
+/* numpy PCG64 state as exposed by Generator.bit_generator.state. */
+typedef struct {
+    uint64_t state_hi, state_lo, inc_hi, inc_lo;
+    int32_t has_uint32;
+    uint32_t uinteger;
+} pw_rng;
+
+/* search.py:76-100 SearchCounters + SearchResult scalars. */
+typedef struct {
+    int64_t iterations, distance_computations, total_visits, nodes_expanded,
+        dgs_skipped, inserted_total;
+    int32_t converged, retained, n_out, pad_;
+    int64_t n_visited;
+} pw_search_out;
+
+const char* pw_last_error(void);
+const char* pw_version(void);
+
+/* Replaces pipeline.py:121-155 build_contexts (one shard; uploads to the
+ * current CUDA device).  Ghost vectors are gathered on the device from
+ * vectors[ghost_ids] (pipeline.py:139-144). */
+int pw_shard_create(const pw_shard_desc* desc, pw_shard** out);
+int pw_shard_destroy(pw_shard* shard);
+/* device memory footprint of a shard in bytes */
+int64_t pw_shard_bytes(const pw_shard* shard);
+
+/* Replaces search.py:269-335 search(query, ctx, params, seeds, rng=...) and,
+ * with use_ghost=1, the inner search of pipeline.py:158-184
+ * run_ghost_stage (params must already be the ghost params).
+ * Host buffers; rng is advanced exactly as numpy would advance it.
+ * out_ids/out_dists/out_local: k entries; visit_log: visit_cap entries. */
+int pw_search_one(pw_shard* shard, int32_t use_ghost, const pw_params* params,
+                  const float* query, const int64_t* seeds, int32_t n_seeds,
+                  pw_rng* rng, int32_t* out_ids, float* out_dists, int32_t* out_local,
+                  pw_search_out* out, int32_t* visit_log, int64_t visit_cap);
+
+/* One pipeline stage for a contiguous query range on one shard -- the
+ * per-(GPU, stage) launch of pipeline.py:329-342 `process` (pipelined) and
+ * :294-297 `do` (baseline).  ALL pointers are DEVICE pointers.
+ *   queries      (q_total, d) float32; rows [q0, q0+n) are searched
+ *   entries_in   (q_total,) int32 entry ids in this shard, or NULL (stage 0 / baseline)
+ *   forward_out  (q_total,) int32 <- inter_map[top1], or NULL (last stage)
+ *   shard_ids/shard_dists (q_total, n_cols, k) written at column `col`
+ *   stats_i32 (4, q_total): iterations, ghost_iterations, retained, converged
+ *   stats_i64 (4, q_total): distance_computations, total_visits, inserted, dgs_skipped
+ * Counters accumulate (+=) like pipeline.py:224-243; converged is assigned.
+ * stream: cudaStream_t (NULL = legacy default stream). */
+int pw_search_stage(pw_shard* shard, const pw_params* params, const pw_tuning* tuning,
+                    const float* queries, int64_t q0, int64_t n, int32_t stage,
+                    const int32_t* entries_in, int32_t* forward_out,
+                    int32_t* shard_ids, float* shard_dists, int32_t n_cols, int32_t col,
+                    int32_t* stats_i32, int64_t* stats_i64, int64_t q_total, void* stream);
+
+/* pipeline.py:187-196 reduce_topk + :249-267 finish over device arrays:
+ * (q, n_cols, k) -> (q, k), by (sqrt'd float32 distance, global id).
+ * Returns PW_EINVAL "cannot reduce empty candidate lists" if some query has
+ * no valid candidate. */
+int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q,
+                   int32_t n_cols, int32_t k, int32_t* final_ids, float* final_dists,
+                   void* stream);
+
+/* Replaces pipeline.py:270-305 run_sharded_baseline (mode 0) and
+ * :308-350 run_pipelined (mode 1) for n_shards shards resident on the
+ * current device (logical shards; the multi-GPU ring lives in the host
+ * layer).  HOST buffers in and out: queries (q, d); shard_ids/dists (q, N, k);
+ * final_ids/dists (q, k); stats_i32/i64 (N, 4, q) as in pw_search_stage;
+ * comm (N, N) int64 bytes per (stage, sending shard). */
+int pw_run(pw_shard* const* shards, int32_t n_shards, const pw_params* params,
+           const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
+           int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
+           int32_t* stats_i32, int64_t* stats_i64, int64_t* comm);
+
+/* Kernel-only timing hook used by bench.py: device-resident variant of
+ * pw_run (all pointers device; no host copies, no synchronisation). */
+int pw_run_device(pw_shard* const* shards, int32_t n_shards, const pw_params* params,
+                  const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
+                  int32_t* shard_ids, float* shard_dists, int32_t* final_ids,
+                  float* final_dists, int32_t* stats_i32, int64_t* stats_i64,
+                  int32_t* entries_a, int32_t* entries_b, void* stream);
+
+/* Bit-exact data.py:70-79 squared_l2 of rows[ids] against one query, on the
+ * device (test hook for the distance primitive).  Device pointers. */
+int pw_squared_l2_rows(pw_shard* shard, const int32_t* ids, int64_t n_ids,
+                       const float* query, float* out, void* stream);
+
+/* Number of kernel launches issued by this library since load (evidence for
+ * bench.py's gpu_launches). */
+int64_t pw_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

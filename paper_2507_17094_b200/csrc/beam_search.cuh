@@ -1,0 +1,742 @@
+// beam_search.cuh -- K1: persistent warp-per-query beam search for sm_100a.
+//
+// One warp runs one whole search (shardann/search.py:269-335) with its state
+// in shared memory: the size-l priority queue (64-bit keys f32bits<<32 | id,
+// which order exactly like the reference's (distance, id) tuples), an exact
+// open-addressing visited set (spilling to a per-warp global table if it
+// fills up), the candidate batch, and a gather staging ring.  Vector rows are
+// gathered with cp.async (LDGSTS) into padded shared-memory rows and reduced
+// in numpy's pairwise float32 order (8 strided accumulators per <=128-element
+// leaf, xor-shuffle tree 1/2/4, sequential tail; recursive halves above 128),
+// so every distance is bit-identical to shardann/data.py:70-79.
+//
+// Per iteration: score new candidates (gather + L2) -> threshold-filter +
+// rank-merge into the queue (search.py:170-190) -> first r unexpanded
+// parents (:192-204) -> one async round trip for adjacency rows, and when
+// pruning the parents' rows + direction rows (direction-guided selection
+// fused as a pre-filter, search.py:249-263) -> ordered in-batch dedup + cap
+// (:230-232, :264) -> visited filter.  Ghost staging (pipeline.py:158-184)
+// runs as a prologue search on the shard's ghost graph in the same warp.
+#pragma once
+#include <stdint.h>
+
+#include "rng_pcg64.cuh"
+
+namespace pw {
+
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr int kMaxLeaves = 64;
+constexpr int kMaxOps = 2 * kMaxLeaves;
+constexpr int kParentGroup = 8;
+
+struct GraphDev {
+    const float* vec;       // (n, d) f32 rows
+    const int32_t* adj;     // (n, j)
+    const int32_t* gid;     // (n,) output id map
+    const uint32_t* dir;    // (n, j, W) or null
+    int32_t n;
+    int32_t j;
+};
+
+// Host-derived per-search configuration (search.py:289-295, direction.py).
+struct SearchCfg {
+    int32_t k, L, want, r, max_iter, cap;
+    int32_t prune_sel;      // 0 none, 1 direction, 2 random
+    int32_t n_keep;         // keep_count(j, discard_ratio)
+    int32_t cool_start;     // first iteration of the full-expansion tail
+    int32_t log;            // log_visits
+};
+
+// Exact numpy pairwise-sum plan for one row length d.
+struct L2Plan {
+    int32_t n_leaves, n_ops;
+    int16_t leaf_off[kMaxLeaves];
+    int16_t leaf_len[kMaxLeaves];
+    int8_t ops[kMaxOps];    // >=0 push leaf i; -1 add top two
+};
+
+struct TaskRecord {         // per-task outputs of pw_search_one
+    int64_t c[6];           // iterations, dc, total_visits, nodes_expanded, dgs, inserted
+    int32_t converged, retained, n_out, pad;
+    int64_t n_visited;
+};
+
+struct KArgs {
+    GraphDev main, ghost;
+    const int32_t* inter;   // (n,) or null
+    int32_t d, W;
+    int32_t spad;           // staging row stride in floats (== 8 mod 32)
+    L2Plan plan;
+    SearchCfg cfg, gcfg;
+    int32_t ghost_on;       // run the ghost prologue when the task has no entry
+    int32_t seed_mode;      // 0 neighbors, 1 mixed
+    int32_t use_ghost_graph;
+    uint64_t seed;
+    int32_t stage;
+    int64_t q0;             // first query id (RNG stream id)
+    int32_t n_tasks;
+    const float* queries;   // row t = task t
+    const int32_t* entries; // per task or null
+    int32_t* forward;       // per task or null
+    const int64_t* seeds;   // explicit seed list (single search) or null
+    int32_t n_seeds;
+    Pcg64* rng_io;          // explicit rng state per task (single search) or null
+    int32_t* out_ids;       // row t at t*out_stride
+    float* out_dists;
+    int32_t* out_local;     // may be null
+    int64_t out_stride;
+    int32_t* st32;          // [f*st_stride + t] (task-relative base) or null
+    int64_t* st64;
+    int64_t st_stride;
+    TaskRecord* rec;        // or null
+    int32_t* visit_log;
+    int64_t visit_cap;
+    // per-warp shared-memory layout (bytes)
+    int32_t L_max, CB, BH, H, R, PG;
+    int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
+        o_misc, warp_bytes;
+    int32_t vis_limit;      // smem visited entries before spilling to global
+    uint32_t* gvis;         // per-warp global visited tables
+    int32_t gmask;
+    uint32_t* gscratch;     // per-warp global scratch for choice()
+    int64_t gscratch_words;
+    int32_t* task_counter;
+    int32_t* err;
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ uint32_t hash32(uint32_t x) { return x * 0x9E3779B1u; }
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Warp-cooperative async copy of `bytes` (multiple of 4) into shared memory.
+__device__ __forceinline__ void warp_copy_async(void* dst, const void* src, int bytes) {
+    const unsigned lane = lane_id();
+    uintptr_t a = (uintptr_t)src | (uintptr_t)__cvta_generic_to_shared(dst);
+    if (((a | (uintptr_t)bytes) & 15u) == 0) {
+        for (int c = lane; c < (bytes >> 4); c += 32)
+            cp_async16((char*)dst + 16 * c, (const char*)src + 16 * c);
+    } else if (((a | (uintptr_t)bytes) & 7u) == 0) {
+        for (int c = lane; c < (bytes >> 3); c += 32)
+            cp_async8((char*)dst + 8 * c, (const char*)src + 8 * c);
+    } else {
+        for (int c = lane; c < (bytes >> 2); c += 32)
+            cp_async4((char*)dst + 4 * c, (const char*)src + 4 * c);
+    }
+}
+
+__device__ __forceinline__ float sqd(float x, float q) {
+    float df = __fsub_rn(x, q);
+    return __fmul_rn(df, df);
+}
+
+// numpy pairwise_sum leaf over squared differences, lanes (v, a=lane&7)
+// hold accumulator a; every lane of the 8-lane group ends with the leaf sum.
+__device__ __forceinline__ float l2_leaf(const float* x, const float* q, int off, int len,
+                                         unsigned a) {
+    if (len < 8) {
+        float s = 0.f;
+        for (int i = 0; i < len; i++) s = __fadd_rn(s, sqd(x[off + i], q[off + i]));
+        return s;
+    }
+    const int nf = len - (len & 7);
+    float acc = sqd(x[off + a], q[off + a]);
+    for (int i = off + (int)a + 8; i < off + nf; i += 8) acc = __fadd_rn(acc, sqd(x[i], q[i]));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
+    acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
+    for (int i = off + nf; i < off + len; i++) acc = __fadd_rn(acc, sqd(x[i], q[i]));
+    return acc;
+}
+
+__device__ __forceinline__ float l2_row(const L2Plan& P, const float* x, const float* q,
+                                        unsigned a) {
+    if (P.n_leaves == 1) return l2_leaf(x, q, 0, P.leaf_len[0], a);
+    float stack[8];
+    int sp = 0;
+    for (int o = 0; o < P.n_ops; o++) {
+        int op = P.ops[o];
+        if (op >= 0) {
+            stack[sp++] = l2_leaf(x, q, P.leaf_off[op], P.leaf_len[op], a);
+        } else {
+            float b = stack[--sp];
+            float t = stack[--sp];
+            stack[sp++] = __fadd_rn(t, b);
+        }
+    }
+    return stack[0];
+}
+
+// --------------------------------------------------------------- per warp
+struct WarpState {
+    float* q;
+    uint64_t* qk[2];
+    uint8_t* qe[2];
+    int32_t* cand;
+    int32_t* cslot;
+    int32_t* newl;
+    uint64_t* ckey;
+    uint32_t* bhk;
+    int32_t* bhp;
+    uint32_t* vh;
+    float* stage;
+    int32_t* misc;
+    uint32_t* gvis;
+    uint32_t* gscr;
+    int32_t cur;            // current queue buffer
+    int32_t qlen;
+    int32_t vcount;         // entries in the smem visited table
+    bool ovf;               // visited set spilled to the global table
+    int64_t c_it, c_dc, c_tv, c_ne, c_dgs, c_ins;
+};
+
+__device__ __forceinline__ uint32_t bh_insert(const KArgs& A, WarpState& S, uint32_t id) {
+    const uint32_t mask = (uint32_t)A.BH - 1u;
+    uint32_t h = hash32(id) & mask;
+    while (true) {
+        uint32_t old = atomicCAS(&S.bhk[h], kEmpty, id);
+        if (old == kEmpty || old == id) return h;
+        h = (h + 1u) & mask;
+    }
+}
+
+__device__ __forceinline__ bool bh_contains(const KArgs& A, const WarpState& S, uint32_t id) {
+    const uint32_t mask = (uint32_t)A.BH - 1u;
+    uint32_t h = hash32(id) & mask;
+    while (true) {
+        uint32_t v = S.bhk[h];
+        if (v == id) return true;
+        if (v == kEmpty) return false;
+        h = (h + 1u) & mask;
+    }
+}
+
+__device__ __forceinline__ void bh_clear(const KArgs& A, WarpState& S) {
+    for (int i = lane_id(); i < A.BH; i += 32) {
+        S.bhk[i] = kEmpty;
+        S.bhp[i] = 0x7FFFFFFF;
+    }
+    __syncwarp();
+}
+
+// Ordered first-occurrence dedup of src[0..n) keeping the first `limit`
+// unique ids, written to dst (search.py:219 dict.fromkeys / :230-232
+// _ordered_unique + [:cap]).  Returns the kept count; bh stays populated.
+__device__ int dedup_ordered(const KArgs& A, WarpState& S, const int32_t* src, int n, int limit,
+                             int32_t* dst, int* n_unique) {
+    const unsigned lane = lane_id();
+    for (int t = lane; t < n; t += 32) {
+        uint32_t slot = bh_insert(A, S, (uint32_t)src[t]);
+        atomicMin(&S.bhp[slot], t);
+        S.cslot[t] = (int32_t)slot;
+    }
+    __syncwarp();
+    int cnt = 0;
+    for (int base = 0; base < n; base += 32) {
+        int t = base + lane;
+        bool f = t < n && S.bhp[S.cslot[t]] == t;
+        unsigned b = __ballot_sync(0xffffffffu, f);
+        int pos = cnt + __popc(b & lanemask_lt());
+        if (f && pos < limit) dst[pos] = src[t];
+        cnt += __popc(b);
+    }
+    __syncwarp();
+    *n_unique = cnt;
+    return cnt < limit ? cnt : limit;
+}
+
+// Exact visited-set insert-if-absent (search.py:167, :300-303).
+__device__ __forceinline__ bool visit_insert(const KArgs& A, WarpState& S, uint32_t id) {
+    const uint32_t hm = (uint32_t)A.H - 1u;
+    uint32_t h = hash32(id) & hm;
+    while (true) {
+        uint32_t v = S.vh[h];
+        if (v == id) return false;
+        if (v == kEmpty) break;
+        h = (h + 1u) & hm;
+    }
+    if (!S.ovf) {
+        while (true) {
+            uint32_t old = atomicCAS(&S.vh[h], kEmpty, id);
+            if (old == kEmpty) return true;
+            if (old == id) return false;
+            h = (h + 1u) & hm;
+        }
+    }
+    const uint32_t gm = (uint32_t)A.gmask;
+    uint32_t g = (hash32(id ^ 0x5bd1e995u) >> 3) & gm;
+    while (true) {
+        uint32_t old = atomicCAS(&S.gvis[g], kEmpty, id);
+        if (old == kEmpty) return true;
+        if (old == id) return false;
+        g = (g + 1u) & gm;
+    }
+}
+
+// Keep only never-scored ids of newl[0..nb) (in order); returns n_new.
+__device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
+    const unsigned lane = lane_id();
+    if (!S.ovf && S.vcount + nb > A.vis_limit) {
+        S.ovf = true;
+        for (int i = lane; i <= A.gmask; i += 32) S.gvis[i] = kEmpty;
+        __syncwarp();
+    }
+    int cnt = 0;
+    for (int base = 0; base < nb; base += 32) {
+        int t = base + lane;
+        int32_t id = t < nb ? S.newl[t] : -1;
+        bool f = t < nb && visit_insert(A, S, (uint32_t)id);
+        unsigned b = __ballot_sync(0xffffffffu, f);
+        int pos = cnt + __popc(b & lanemask_lt());
+        if (f) S.newl[pos] = id;
+        cnt += __popc(b);
+    }
+    __syncwarp();
+    if (!S.ovf) S.vcount += cnt;
+    return cnt;
+}
+
+// Gather rows newl[0..n) and compute exact squared L2 keys into ckey.
+__device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n) {
+    const unsigned lane = lane_id();
+    const int RH = A.R >> 1;
+    const int row_bytes = A.d * 4;
+    const int sp = A.spad;
+    const int ngroups = (n + RH - 1) / RH;
+    auto issue = [&](int g) {
+        if (g < ngroups) {
+            int r0 = g * RH;
+            int rows = min(RH, n - r0);
+            float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
+            for (int r = 0; r < rows; r++) {
+                int32_t id = S.newl[r0 + r];
+                warp_copy_async(dst0 + (size_t)r * sp, G.vec + (size_t)id * A.d, row_bytes);
+            }
+        }
+        cp_commit();
+    };
+    issue(0);
+    issue(1);
+    const unsigned v = lane >> 3, a = lane & 7u;
+    for (int g = 0; g < ngroups; g++) {
+        cp_wait<1>();
+        __syncwarp();
+        int r0 = g * RH;
+        int rows = min(RH, n - r0);
+        const float* base = S.stage + (size_t)(g & 1) * RH * sp;
+        for (int sub = 0; sub < rows; sub += 4) {
+            int rr = sub + (int)v;
+            int rc = rr < rows ? rr : rows - 1;
+            float dist = l2_row(A.plan, base + (size_t)rc * sp, S.q, a);
+            if (a == 0 && rr < rows) {
+                uint32_t id = (uint32_t)S.newl[r0 + rr];
+                S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
+            }
+        }
+        __syncwarp();
+        issue(g + 2);
+    }
+    cp_wait<0>();
+    __syncwarp();
+}
+
+// search.py:170-190 merge_and_sort on keys; returns `inserted`.
+__device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int n) {
+    const unsigned lane = lane_id();
+    const int L = C.L;
+    const uint64_t* qk = S.qk[S.cur];
+    const uint8_t* qe = S.qe[S.cur];
+    uint64_t* nk = S.qk[S.cur ^ 1];
+    uint8_t* ne = S.qe[S.cur ^ 1];
+    const int qlen = S.qlen;
+    const uint64_t thr = qlen == L ? qk[L - 1] : ~0ull;
+    // survivors (compacted in place in ckey)
+    int s = 0;
+    for (int base = 0; base < n; base += 32) {
+        int t = base + lane;
+        uint64_t key = t < n ? S.ckey[t] : ~0ull;
+        bool f = t < n && key < thr;
+        unsigned b = __ballot_sync(0xffffffffu, f);
+        int pos = s + __popc(b & lanemask_lt());
+        if (f) S.ckey[pos] = key;
+        s += __popc(b);
+    }
+    __syncwarp();
+    if (s == 0) return 0;
+    // queue entries: shift by number of smaller survivors
+    for (int t = lane; t < qlen; t += 32) {
+        uint64_t key = qk[t];
+        int sh = 0;
+        for (int i = 0; i < s; i++) sh += S.ckey[i] < key;
+        int np = t + sh;
+        if (np < L) {
+            nk[np] = key;
+            ne[np] = qe[t];
+        }
+    }
+    // survivors: rank among survivors + lower_bound in the queue
+    int ins = 0;
+    for (int base = 0; base < s; base += 32) {
+        int i = base + lane;
+        bool kept = false;
+        if (i < s) {
+            uint64_t key = S.ckey[i];
+            int rs = 0;
+            for (int o = 0; o < s; o++) rs += S.ckey[o] < key;
+            int lo = 0, hi = qlen;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (qk[mid] < key) lo = mid + 1;
+                else hi = mid;
+            }
+            int p = rs + lo;
+            if (p < L) {
+                nk[p] = key;
+                ne[p] = 0;
+                kept = true;
+            }
+        }
+        ins += __popc(__ballot_sync(0xffffffffu, kept));
+    }
+    __syncwarp();
+    S.qlen = min(L, qlen + s);
+    S.cur ^= 1;
+    return ins;
+}
+
+// search.py:192-204: first r unexpanded queue entries, marked expanded.
+__device__ int select_parents(WarpState& S, int r, int32_t* parents) {
+    const unsigned lane = lane_id();
+    uint64_t* qk = S.qk[S.cur];
+    uint8_t* qe = S.qe[S.cur];
+    int np = 0;
+    for (int base = 0; base < S.qlen && np < r; base += 32) {
+        int t = base + lane;
+        bool f = t < S.qlen && qe[t] == 0;
+        unsigned b = __ballot_sync(0xffffffffu, f);
+        int pos = np + __popc(b & lanemask_lt());
+        if (f && pos < r) {
+            parents[pos] = (int32_t)(uint32_t)qk[t];
+            qe[t] = 1;
+        }
+        np = min(r, np + __popc(b));
+    }
+    __syncwarp();
+    return np;
+}
+
+// _expand (search.py:235-266) up to the ordered candidate list in S.cand;
+// returns the candidate count p * n_sel.
+__device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
+                      const int32_t* parents, int np, int it, Pcg64& rng) {
+    const unsigned lane = lane_id();
+    const int j = G.j;
+    if (j == 0) return 0;
+    const bool prune = C.prune_sel != 0 && it < C.cool_start;
+    if (!prune) {
+        for (int pi = 0; pi < np; pi++)
+            warp_copy_async(S.cand + pi * j, G.adj + (size_t)parents[pi] * j, j * 4);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        return np * j;
+    }
+    const int nsel = C.n_keep < j ? C.n_keep : j;
+    int32_t* craw = reinterpret_cast<int32_t*>(S.ckey);  // free during expansion
+    int32_t* cnt = S.misc;                                // PG * j
+    int32_t* perm = S.misc;                               // j (random arm)
+    uint32_t* qb = reinterpret_cast<uint32_t*>(S.misc + A.PG * j);  // PG * W
+    if (C.prune_sel == 1) {
+        const int W = A.W, d = A.d;
+        for (int pg = 0; pg < np; pg += A.PG) {
+            const int gp = min(A.PG, np - pg);
+            float* prow = S.stage;
+            uint32_t* drow = reinterpret_cast<uint32_t*>(S.stage + (size_t)gp * A.spad);
+            for (int pi = 0; pi < gp; pi++) {
+                const int32_t par = parents[pg + pi];
+                warp_copy_async(craw + (pg + pi) * j, G.adj + (size_t)par * j, j * 4);
+                warp_copy_async(prow + (size_t)pi * A.spad, G.vec + (size_t)par * d, d * 4);
+                warp_copy_async(drow + (size_t)pi * j * W, G.dir + (size_t)par * j * W, j * W * 4);
+            }
+            cp_commit();
+            cp_wait<0>();
+            __syncwarp();
+            // query direction bits pack(q >= x_parent) (direction.py:53-59)
+            for (int pi = 0; pi < gp; pi++)
+                for (int w = 0; w < W; w++) {
+                    int t = 32 * w + (int)lane;
+                    bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
+                    unsigned word = __ballot_sync(0xffffffffu, bit);
+                    if (lane == 0) qb[pi * W + w] = word;
+                }
+            __syncwarp();
+            // matching counts d - popc(dir ^ qbits) (direction.py:62-69)
+            for (int pi = 0; pi < gp; pi++)
+                for (int s = lane; s < j; s += 32) {
+                    int diff = 0;
+                    const uint32_t* dr = drow + ((size_t)pi * j + s) * W;
+                    for (int w = 0; w < W; w++) diff += __popc(dr[w] ^ qb[pi * W + w]);
+                    cnt[pi * j + s] = d - diff;
+                }
+            __syncwarp();
+            // stable argsort(-counts)[:n_keep] (direction.py:79-87)
+            for (int pi = 0; pi < gp; pi++)
+                for (int s = lane; s < j; s += 32) {
+                    int c = cnt[pi * j + s];
+                    int rank = 0;
+                    for (int o = 0; o < j; o++) {
+                        int co = cnt[pi * j + o];
+                        rank += (co > c) || (co == c && o < s);
+                    }
+                    if (rank < nsel) S.cand[(pg + pi) * nsel + rank] = craw[(pg + pi) * j + s];
+                }
+            __syncwarp();
+        }
+    } else {
+        for (int pi = 0; pi < np; pi++)
+            warp_copy_async(craw + pi * j, G.adj + (size_t)parents[pi] * j, j * 4);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        for (int pi = 0; pi < np; pi++) {
+            if (lane == 0) permutation(rng, (uint32_t)j, perm);  // direction.py:103-105
+            __syncwarp();
+            for (int t = lane; t < nsel; t += 32) S.cand[pi * nsel + t] = craw[pi * j + perm[t]];
+            __syncwarp();
+        }
+    }
+    S.c_dgs += (int64_t)np * (j - C.n_keep);
+    return np * nsel;
+}
+
+// One full search (search.py:269-335) over graph G.  Seeds (already in
+// S.cand[0..ns)) are deduplicated in order and capped at `want`; the
+// random fill draws Generator.choice(n, want) from rng.
+__device__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
+                           int ns, bool fill_random, Pcg64& rng, int64_t task,
+                           int64_t* n_logged) {
+    const unsigned lane = lane_id();
+    // reset per-search state
+    for (int i = lane; i < A.H; i += 32) S.vh[i] = kEmpty;
+    bh_clear(A, S);
+    S.cur = 0;
+    S.qlen = 0;
+    S.vcount = 0;
+    S.ovf = false;
+    S.c_it = S.c_dc = S.c_tv = S.c_ne = S.c_dgs = S.c_ins = 0;
+
+    // _initial_batch (search.py:207-227)
+    int nuniq;
+    int nb = dedup_ordered(A, S, S.cand, ns, C.want, S.newl, &nuniq);
+    if (fill_random && nb < C.want) {
+        int32_t* ch = S.cand;
+        if (lane == 0) {
+            const uint32_t pop = (uint32_t)G.n, size = (uint32_t)C.want;
+            if (choice_uses_tail(pop, size)) {
+                uint32_t cap = 1;
+                while (cap < 4u * size + 8u) cap <<= 1;
+                choice_tail(rng, pop, size, S.gscr, S.gscr + cap, cap - 1, ch);
+            } else {
+                uint32_t mask = (uint32_t)gen_mask64((uint64_t)(1.2 * (double)size));
+                uint32_t* set = ((int64_t)(mask + 1) * 4 <= (int64_t)A.R * A.spad * 4)
+                                    ? reinterpret_cast<uint32_t*>(S.stage)
+                                    : S.gscr;
+                choice_floyd(rng, pop, size, set, mask, ch);
+            }
+        }
+        __syncwarp();
+        int cnt = nb;
+        for (int base = 0; base < C.want && cnt < C.want; base += 32) {
+            int t = base + lane;
+            int32_t id = t < C.want ? ch[t] : -1;
+            bool f = t < C.want && !bh_contains(A, S, (uint32_t)id);
+            unsigned b = __ballot_sync(0xffffffffu, f);
+            int pos = cnt + __popc(b & lanemask_lt());
+            if (f && pos < C.want) S.newl[pos] = id;
+            cnt = min(C.want, cnt + __popc(b));
+        }
+        __syncwarp();
+        nb = cnt;
+    }
+    bh_clear(A, S);
+    int n_new = visited_filter(A, S, nb);
+
+    bool converged = false;
+    int32_t* parents = S.misc + A.PG * G.j + A.PG * A.W + 8;
+    for (int it = 0; it < C.max_iter; it++) {
+        S.c_it++;
+        int inserted = 0;
+        if (n_new) {
+            if (C.log && A.visit_log) {
+                for (int t = lane; t < n_new; t += 32) {
+                    int64_t p = *n_logged + t;
+                    if (p < A.visit_cap) A.visit_log[task * A.visit_cap + p] = S.newl[t];
+                }
+                *n_logged += n_new;
+            }
+            S.c_dc += n_new;
+            score_rows(A, S, G, n_new);
+            inserted = merge_queue(A, S, C, n_new);
+            S.c_ins += inserted;
+        }
+        if (inserted == 0) {
+            converged = true;
+            break;
+        }
+        if (it == C.max_iter - 1) break;
+        int np = select_parents(S, C.r, parents);
+        if (np == 0) {
+            converged = true;
+            break;
+        }
+        S.c_ne += np;
+        int nc = expand(A, S, G, C, parents, np, it, rng);
+        nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
+        S.c_tv += nb;
+        bh_clear(A, S);
+        n_new = visited_filter(A, S, nb);
+    }
+    return converged;
+}
+
+__global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
+    unsigned char* base = smem_raw + (size_t)warp * A.warp_bytes;
+    WarpState S;
+    S.q = reinterpret_cast<float*>(base + A.o_q);
+    S.qk[0] = reinterpret_cast<uint64_t*>(base + A.o_qk);
+    S.qk[1] = S.qk[0] + A.L_max;
+    S.qe[0] = reinterpret_cast<uint8_t*>(base + A.o_qe);
+    S.qe[1] = S.qe[0] + A.L_max;
+    S.cand = reinterpret_cast<int32_t*>(base + A.o_cand);
+    S.cslot = reinterpret_cast<int32_t*>(base + A.o_cslot);
+    S.newl = reinterpret_cast<int32_t*>(base + A.o_newl);
+    S.ckey = reinterpret_cast<uint64_t*>(base + A.o_ckey);
+    S.bhk = reinterpret_cast<uint32_t*>(base + A.o_bhk);
+    S.bhp = reinterpret_cast<int32_t*>(base + A.o_bhp);
+    S.vh = reinterpret_cast<uint32_t*>(base + A.o_vh);
+    S.stage = reinterpret_cast<float*>(base + A.o_stage);
+    S.misc = reinterpret_cast<int32_t*>(base + A.o_misc);
+    S.gvis = A.gvis + (size_t)gwarp * (A.gmask + 1);
+    S.gscr = A.gscratch + (size_t)gwarp * A.gscratch_words;
+
+    while (true) {
+        int task = 0;
+        if (lane == 0) task = atomicAdd(A.task_counter, 1);
+        task = __shfl_sync(0xffffffffu, task, 0);
+        if (task >= A.n_tasks) break;
+        const int64_t qid = A.q0 + task;
+        // query row -> smem
+        for (int t = lane; t < A.d; t += 32) S.q[t] = A.queries[(size_t)task * A.d + t];
+        __syncwarp();
+
+        int32_t g_it = 0;
+        int64_t g_dc = 0, g_tv = 0;
+        int64_t n_logged = 0;
+        bool has_entry = A.entries != nullptr;
+        int32_t entry = has_entry ? A.entries[task] : -1;
+        const GraphDev& G = A.use_ghost_graph ? A.ghost : A.main;
+
+        // ghost staging prologue (pipeline.py:218-226)
+        if (!has_entry && A.n_seeds == 0 && A.ghost_on) {
+            Pcg64 grng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)A.stage));
+            run_search(A, S, A.ghost, A.gcfg, 0, true, grng, task, &n_logged);
+            entry = A.ghost.gid[(uint32_t)S.qk[S.cur][0]];
+            has_entry = true;
+            g_it = (int32_t)S.c_it;
+            g_dc = S.c_dc;
+            g_tv = S.c_tv;
+            n_logged = 0;
+        }
+        // seeds (pipeline.py:227-231, search.py:294)
+        int ns = 0;
+        bool fill_random;
+        if (A.n_seeds > 0) {
+            for (int t = lane; t < A.n_seeds; t += 32) S.cand[t] = (int32_t)A.seeds[t];
+            ns = A.n_seeds;
+            fill_random = A.seed_mode == 1;
+        } else if (has_entry) {
+            if (lane == 0) S.cand[0] = entry;
+            ns = 1;
+            if (A.seed_mode == 0) {
+                for (int t = lane; t < G.j; t += 32) S.cand[1 + t] = G.adj[(size_t)entry * G.j + t];
+                ns = 1 + G.j;
+                fill_random = false;
+            } else {
+                fill_random = true;
+            }
+        } else {
+            fill_random = true;
+        }
+        __syncwarp();
+        Pcg64 rng = A.rng_io ? A.rng_io[task]
+                             : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)A.stage));
+        const bool converged = run_search(A, S, G, A.cfg, ns, fill_random, rng, task, &n_logged);
+        if (A.rng_io && lane == 0) A.rng_io[task] = rng;
+
+        // outputs (search.py:323-335, pipeline.py:236-246, :339)
+        const uint64_t* qk = S.qk[S.cur];
+        const int nk = min(S.qlen, A.cfg.k);
+        for (int t = lane; t < nk; t += 32) {
+            uint64_t key = qk[t];
+            uint32_t loc = (uint32_t)key;
+            A.out_ids[task * A.out_stride + t] = G.gid[loc];
+            A.out_dists[task * A.out_stride + t] = __fsqrt_rn(__uint_as_float((uint32_t)(key >> 32)));
+            if (A.out_local) A.out_local[task * A.out_stride + t] = (int32_t)loc;
+        }
+        if (lane == 0) {
+            if (A.forward && nk > 0) A.forward[task] = A.inter[(uint32_t)qk[0]];
+            if (A.st32) {
+                A.st32[0 * A.st_stride + task] += (int32_t)S.c_it;
+                A.st32[1 * A.st_stride + task] += g_it;
+                A.st32[2 * A.st_stride + task] += S.qlen;
+                A.st32[3 * A.st_stride + task] = converged ? 1 : 0;
+                A.st64[0 * A.st_stride + task] += S.c_dc + g_dc;
+                A.st64[1 * A.st_stride + task] += S.c_tv + g_tv;
+                A.st64[2 * A.st_stride + task] += S.c_ins;
+                A.st64[3 * A.st_stride + task] += S.c_dgs;
+            }
+            if (A.rec) {
+                TaskRecord& R = A.rec[task];
+                R.c[0] = S.c_it;
+                R.c[1] = S.c_dc;
+                R.c[2] = S.c_tv;
+                R.c[3] = S.c_ne;
+                R.c[4] = S.c_dgs;
+                R.c[5] = S.c_ins;
+                R.converged = converged ? 1 : 0;
+                R.retained = S.qlen;
+                R.n_out = nk;
+                R.n_visited = n_logged;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace pw

@@ -1,0 +1,749 @@
+// pw_abi.cu -- host side of the C ABI (include/pw_b200.h) + K2 reduce_topk.
+//
+// Owns device copies of shards (pipeline.py:121-155 build_contexts), derives
+// per-search configuration from SearchParams exactly as search.py:289-295
+// and direction.py:72-100 do, sizes the per-warp shared-memory layout of the
+// beam-search kernel, and drives stages (pipeline.py:270-350).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/pw_b200.h"
+#include "beam_search.cuh"
+
+using namespace pw;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define PW_CUDA(call)                                                                  \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return set_err(e_ == cudaErrorMemoryAllocation ? PW_ENOMEM : PW_ECUDA,     \
+                           std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+int words_per_vector(int d) { return (d + 31) / 32; }
+int pw_fill_inf(float* p, int64_t n, cudaStream_t st);
+
+int32_t keep_count(int32_t j, double discard) {  // direction.py:72-76
+    int32_t v = (int32_t)((1.0 - discard) * (double)j + 0.5);
+    return v > 1 ? v : 1;
+}
+int32_t cooldown_start(int32_t max_iter, double ratio) {  // direction.py:90-100
+    return max_iter - (int32_t)std::floor(ratio * (double)max_iter + 1e-9);
+}
+int64_t next_pow2(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+// numpy pairwise_sum structure (loops_utils.h.src): leaves of <= 128
+// elements, split at n2 = n/2 - (n/2)%8; postfix ops for the device stack.
+void plan_rec(L2Plan& P, int off, int n) {
+    if (n <= 128) {
+        int i = P.n_leaves++;
+        P.leaf_off[i] = (int16_t)off;
+        P.leaf_len[i] = (int16_t)n;
+        P.ops[P.n_ops++] = (int8_t)i;
+        return;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    plan_rec(P, off, n2);
+    plan_rec(P, off + n2, n - n2);
+    P.ops[P.n_ops++] = -1;
+}
+
+bool make_plan(int d, L2Plan& P) {
+    std::memset(&P, 0, sizeof P);
+    if (d > 128 * kMaxLeaves / 2 || d > 32767) return false;
+    plan_rec(P, 0, d);
+    return P.n_leaves <= kMaxLeaves && P.n_ops <= kMaxOps;
+}
+
+struct DevInfo {
+    int sms = 0;
+    int smem_optin = 0;
+    bool attr_set = false;
+};
+std::mutex g_dev_mu;
+DevInfo g_dev[64];
+
+int dev_info(int dev, DevInfo** out) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    DevInfo& I = g_dev[dev];
+    if (I.sms == 0) {
+        PW_CUDA(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, dev));
+        PW_CUDA(cudaDeviceGetAttribute(&I.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    }
+    if (!I.attr_set) {
+        PW_CUDA(cudaFuncSetAttribute(beam_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     I.smem_optin));
+        I.attr_set = true;
+    }
+    *out = &I;
+    return 0;
+}
+
+}  // namespace
+
+struct pw_shard {
+    int device = 0;
+    int64_t n = 0;
+    int32_t d = 0, j = 0, W = 0, dtype = 0;
+    float* vec = nullptr;
+    int32_t* adj = nullptr;
+    int32_t* gid = nullptr;
+    uint32_t* dir = nullptr;
+    int32_t* inter = nullptr;
+    int64_t gn = 0;
+    int32_t gj = 0;
+    float* gvec = nullptr;
+    int32_t* gadj = nullptr;
+    int32_t* gids = nullptr;
+    int64_t bytes = 0;
+    // launch workspace (grow-only)
+    int32_t* counter = nullptr;
+    uint32_t* gvis = nullptr;
+    size_t gvis_words = 0;
+    uint32_t* gscr = nullptr;
+    size_t gscr_words = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+template <typename T>
+int upload(T** dst, const void* src, size_t count, int64_t* bytes) {
+    if (count == 0) count = 1;
+    PW_CUDA(cudaMalloc((void**)dst, count * sizeof(T)));
+    if (src) PW_CUDA(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+    *bytes += (int64_t)(count * sizeof(T));
+    return 0;
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ vec, const int32_t* __restrict__ ids,
+                                   int64_t n_ids, int32_t d, float* __restrict__ out) {
+    int64_t total = n_ids * d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / d, c = i % d;
+        out[i] = vec[(int64_t)ids[r] * d + c];
+    }
+}
+
+// K2: per-query best k of n_cols*k candidates by (distance, id)
+// (pipeline.py:187-196).  One warp per query; rank selection in shared memory.
+__global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float* __restrict__ dists,
+                                   int64_t q, int32_t n, int32_t k, int32_t* __restrict__ out_ids,
+                                   float* __restrict__ out_dists, int32_t* err) {
+    extern __shared__ uint64_t rk_keys[];
+    const int warps = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5;
+    const unsigned lane = threadIdx.x & 31u;
+    uint64_t* keys = rk_keys + (size_t)w * n;
+    for (int64_t qi = (int64_t)blockIdx.x * warps + w; qi < q; qi += (int64_t)gridDim.x * warps) {
+        int cnt = 0;
+        for (int base = 0; base < n; base += 32) {
+            int t = base + lane;
+            int32_t id = t < n ? ids[qi * n + t] : -1;
+            bool f = id >= 0;
+            unsigned b = __ballot_sync(0xffffffffu, f);
+            int pos = cnt + __popc(b & lanemask_lt());
+            if (f) keys[pos] = ((uint64_t)__float_as_uint(dists[qi * n + t]) << 32) | (uint32_t)id;
+            cnt += __popc(b);
+        }
+        __syncwarp();
+        if (cnt == 0 && lane == 0) atomicExch(err, 1);
+        for (int t = lane; t < k; t += 32) {
+            out_ids[qi * k + t] = -1;
+            out_dists[qi * k + t] = __int_as_float(0x7f800000);
+        }
+        __syncwarp();
+        for (int t = lane; t < cnt; t += 32) {
+            uint64_t key = keys[t];
+            int rank = 0;
+            for (int o = 0; o < cnt; o++) rank += keys[o] < key;
+            if (rank < k) {
+                out_ids[qi * k + rank] = (int32_t)(uint32_t)key;
+                out_dists[qi * k + rank] = __uint_as_float((uint32_t)(key >> 32));
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Test hook: exact squared L2 of rows[ids] vs query (data.py:70-79).
+__global__ void l2_rows_kernel(const float* __restrict__ vec, int32_t d, int32_t spad, L2Plan plan,
+                               const int32_t* __restrict__ ids, int64_t n_ids,
+                               const float* __restrict__ query, float* __restrict__ out) {
+    extern __shared__ float l2s[];
+    float* q = l2s;
+    float* rows = l2s + ((d + 3) & ~3);
+    const unsigned lane = threadIdx.x & 31u;
+    for (int t = lane; t < d; t += 32) q[t] = query[t];
+    for (int64_t r0 = (int64_t)blockIdx.x * 4; r0 < n_ids; r0 += (int64_t)gridDim.x * 4) {
+        __syncwarp();
+        for (int v = 0; v < 4; v++) {
+            int64_t r = r0 + v < n_ids ? r0 + v : n_ids - 1;
+            for (int t = lane; t < d; t += 32) rows[v * spad + t] = vec[(int64_t)ids[r] * d + t];
+        }
+        __syncwarp();
+        const unsigned v = lane >> 3, a = lane & 7u;
+        float dist = l2_row(plan, rows + v * spad, q, a);
+        if (a == 0 && r0 + v < n_ids) out[r0 + v] = dist;
+    }
+}
+
+SearchCfg make_cfg(const pw_params& p, int64_t n, int32_t j) {
+    SearchCfg c;
+    c.k = p.k;
+    c.L = p.l;
+    c.want = (int32_t)std::min<int64_t>(p.m, n);
+    c.r = p.r;
+    c.max_iter = p.max_iter;
+    c.cap = p.buffer_cap ? p.buffer_cap : std::max(p.m, p.r * j);  // search.py:289
+    c.prune_sel = (p.selection != PW_SEL_FULL && p.discard_ratio > 0.0) ? p.selection : 0;
+    c.n_keep = keep_count(j, p.discard_ratio);
+    c.cool_start = cooldown_start(p.max_iter, p.cooldown_ratio);
+    c.log = p.log_visits;
+    return c;
+}
+
+int validate_params(const pw_params& p) {  // search.py:58-70
+    if (!(1 <= p.k && p.k <= p.l && 1 <= p.r && p.r <= p.l))
+        return set_err(PW_EINVAL, "need k <= l and r <= l, got k=" + std::to_string(p.k) +
+                                      " l=" + std::to_string(p.l) + " r=" + std::to_string(p.r));
+    if (p.m < 1 || p.max_iter < 1 || p.ghost_max_iter < 1)
+        return set_err(PW_EINVAL, "m, max_iter and ghost_max_iter must be >= 1");
+    if (!(0.0 <= p.discard_ratio && p.discard_ratio < 1.0))
+        return set_err(PW_EINVAL, "discard_ratio must be in [0, 1)");
+    if (!(0.0 <= p.cooldown_ratio && p.cooldown_ratio <= 1.0))
+        return set_err(PW_EINVAL, "cooldown_ratio must be in [0, 1]");
+    if (p.selection < 0 || p.selection > 2) return set_err(PW_EINVAL, "selection must be one of ('full', 'direction', 'random')");
+    if (p.seed_mode < 0 || p.seed_mode > 1) return set_err(PW_EINVAL, "seed_mode must be one of ('neighbors', 'mixed')");
+    if (p.buffer_cap < 0) return set_err(PW_EINVAL, "buffer_cap must be positive");
+    return 0;
+}
+
+// Build the launch description (shared-memory layout, configs) for one shard.
+struct Launch {
+    KArgs A;
+    int warps_per_block = 0;
+    int blocks = 0;
+    size_t smem = 0;
+};
+
+int64_t visit_bound(const SearchCfg& c, int32_t j, int64_t n) {
+    int64_t per = std::min<int64_t>(c.cap, (int64_t)c.r * j);
+    int64_t b = c.want + (int64_t)(c.max_iter - 1) * per;
+    return std::min<int64_t>(b, n);
+}
+
+int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_ghost_graph,
+            int32_t n_seeds, bool ghost_on, Launch& Lc) {
+    int rc = validate_params(p);
+    if (rc) return rc;
+    if (sh->dtype != PW_DTYPE_F32) return set_err(PW_EINVAL, "only float32 shards are supported");
+    KArgs& A = Lc.A;
+    std::memset(&A, 0, sizeof A);
+    A.main = GraphDev{sh->vec, sh->adj, sh->gid, sh->dir, (int32_t)sh->n, sh->j};
+    A.ghost = GraphDev{sh->gvec, sh->gadj, sh->gids, nullptr, (int32_t)sh->gn, sh->gj};
+    A.inter = sh->inter;
+    A.d = sh->d;
+    A.W = sh->W;
+    if (!make_plan(sh->d, A.plan)) return set_err(PW_EINVAL, "dimension too large");
+    const GraphDev& G = use_ghost_graph ? A.ghost : A.main;
+    if (use_ghost_graph && sh->gn == 0) return set_err(PW_EINVAL, "ghost index absent for this shard");
+    A.cfg = make_cfg(p, G.n, G.j);
+    pw_params gp = p;  // pipeline.py:174-182
+    gp.k = 1;
+    gp.max_iter = p.ghost_max_iter;
+    gp.selection = PW_SEL_FULL;
+    gp.discard_ratio = 0.0;
+    gp.log_visits = 0;
+    gp.buffer_cap = 0;
+    A.gcfg = make_cfg(gp, std::max<int64_t>(sh->gn, 1), sh->gj);
+    A.ghost_on = ghost_on ? 1 : 0;
+    A.seed_mode = p.seed_mode;
+    A.use_ghost_graph = use_ghost_graph ? 1 : 0;
+    A.seed = p.seed;
+    if (A.cfg.prune_sel == PW_SEL_DIRECTION && !sh->dir)
+        return set_err(PW_EINVAL, "direction table required for direction-guided selection");
+
+    // ---- shared-memory layout per warp
+    const int jm = std::max(G.j, ghost_on ? sh->gj : 0);
+    const int d = sh->d;
+    int spad = (d + 31) / 32 * 32 + 8;  // == 8 mod 32: conflict-free (v, a) access
+    if (spad - 32 >= d) spad -= 32;
+    A.spad = spad;
+    int64_t cb = std::max<int64_t>({(int64_t)p.r * jm, (int64_t)A.cfg.want, (int64_t)1 + jm,
+                                    (int64_t)n_seeds, (int64_t)A.gcfg.want, 32});
+    cb = (cb + 31) / 32 * 32;
+    A.CB = (int32_t)cb;
+    A.BH = (int32_t)next_pow2(2 * cb);
+    A.L_max = p.l;
+    int64_t bound = visit_bound(A.cfg, G.j, G.n);
+    if (ghost_on) bound = std::max(bound, visit_bound(A.gcfg, sh->gj, sh->gn));
+    int64_t H = tun && tun->visited_slots > 0 ? next_pow2(tun->visited_slots)
+                                              : std::min<int64_t>(4096, next_pow2(bound * 4 / 3 + 2));
+    H = std::max<int64_t>(H, 64);
+    A.H = (int32_t)H;
+    A.vis_limit = (int32_t)(H * 3 / 4);
+    int R = tun && tun->stage_rows > 0 ? tun->stage_rows : std::max(2, std::min(16, (16384 / (spad * 4)) & ~1));
+    R &= ~1;
+    if (R < 2) R = 2;
+    int W = sh->W;
+    int PG = 1;
+    if (A.cfg.prune_sel == PW_SEL_DIRECTION) {
+        while ((int64_t)R * spad < (int64_t)spad + (int64_t)G.j * W) R += 2;
+        PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad) / (spad + (int64_t)G.j * W));
+        PG = std::max(PG, 1);
+    }
+    A.R = R;
+    A.PG = PG;
+    auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
+    int64_t off = 0;
+    A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
+    A.o_qk = (int32_t)off; off = al(off + 8 * 2 * (int64_t)p.l);
+    A.o_qe = (int32_t)off; off = al(off + 2 * (int64_t)p.l);
+    A.o_cand = (int32_t)off; off = al(off + 4 * cb);
+    A.o_cslot = (int32_t)off; off = al(off + 4 * cb);
+    A.o_newl = (int32_t)off; off = al(off + 4 * cb);
+    A.o_ckey = (int32_t)off; off = al(off + 8 * cb);
+    A.o_bhk = (int32_t)off; off = al(off + 4 * (int64_t)A.BH);
+    A.o_bhp = (int32_t)off; off = al(off + 4 * (int64_t)A.BH);
+    A.o_vh = (int32_t)off; off = al(off + 4 * H);
+    A.o_stage = (int32_t)off; off = al(off + 4 * (int64_t)R * spad);
+    A.o_misc = (int32_t)off;
+    int64_t misc = (int64_t)std::max(jm, PG * jm) + (int64_t)PG * W + 8 + p.r + 8;
+    off = al(off + 4 * misc);
+    A.warp_bytes = (int32_t)off;
+
+    DevInfo* I;
+    if ((rc = dev_info(sh->device, &I))) return rc;
+    int wpb = (int)std::min<int64_t>(16, I->smem_optin / off);
+    if (tun && tun->warps_per_sm > 0) wpb = std::min(wpb, tun->warps_per_sm);
+    if (wpb < 1) return set_err(PW_EINVAL, "search configuration needs " + std::to_string(off) +
+                                              " bytes of shared memory per query (l or degree too large)");
+    Lc.warps_per_block = wpb;
+    Lc.blocks = I->sms;
+    Lc.smem = (size_t)wpb * off;
+
+    // ---- global workspace: visited spill tables + choice scratch
+    const int total_warps = Lc.blocks * wpb;
+    int64_t gsz = bound > A.vis_limit ? next_pow2(2 * bound + 2) : 1;
+    A.gmask = (int32_t)(gsz - 1);
+    int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
+    int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
+    std::lock_guard<std::mutex> lk(sh->mu);
+    if (!sh->counter) PW_CUDA(cudaMalloc(&sh->counter, sizeof(int32_t) * 2));
+    if (sh->gvis_words < (size_t)total_warps * gsz) {
+        if (sh->gvis) cudaFree(sh->gvis);
+        sh->gvis = nullptr;
+        PW_CUDA(cudaMalloc(&sh->gvis, sizeof(uint32_t) * (size_t)total_warps * gsz));
+        sh->gvis_words = (size_t)total_warps * gsz;
+    }
+    if (sh->gscr_words < (size_t)total_warps * scr) {
+        if (sh->gscr) cudaFree(sh->gscr);
+        sh->gscr = nullptr;
+        PW_CUDA(cudaMalloc(&sh->gscr, sizeof(uint32_t) * (size_t)total_warps * scr));
+        sh->gscr_words = (size_t)total_warps * scr;
+    }
+    A.gvis = sh->gvis;
+    A.gscratch = sh->gscr;
+    A.gscratch_words = scr;
+    A.task_counter = sh->counter;
+    A.err = sh->counter + 1;
+    return 0;
+}
+
+int launch(pw_shard* sh, Launch& Lc, cudaStream_t st) {
+    if (Lc.A.n_tasks <= 0) return 0;
+    PW_CUDA(cudaSetDevice(sh->device));
+    PW_CUDA(cudaMemsetAsync(sh->counter, 0, sizeof(int32_t), st));
+    int blocks = std::min<int64_t>(Lc.blocks, ((int64_t)Lc.A.n_tasks + Lc.warps_per_block - 1) / Lc.warps_per_block);
+    beam_search_kernel<<<blocks, 32 * Lc.warps_per_block, Lc.smem, st>>>(Lc.A);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pw_last_error(void) { return g_err.c_str(); }
+const char* pw_version(void) { return "pwb200 0.1.0 (sm_100a)"; }
+int64_t pw_launch_count(void) { return g_launches.load(); }
+
+int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
+    if (!D || !out) return set_err(PW_EINVAL, "null argument");
+    if (D->n <= 0) return set_err(PW_EINVAL, "empty graph");
+    if (D->n >= (1ll << 31)) return set_err(PW_EINVAL, "shard too large (n_local >= 2^31)");
+    if (D->d < 1 || D->j < 0) return set_err(PW_EINVAL, "bad dimensions");
+    if (D->dtype != PW_DTYPE_F32) return set_err(PW_EINVAL, "only float32 vectors are supported");
+    pw_shard* sh = new pw_shard();
+    int dev = 0;
+    cudaGetDevice(&dev);
+    sh->device = dev;
+    sh->n = D->n;
+    sh->d = D->d;
+    sh->j = D->j;
+    sh->W = words_per_vector(D->d);
+    sh->dtype = D->dtype;
+    int rc = 0;
+    auto fail = [&](int code) {
+        pw_shard_destroy(sh);
+        return code;
+    };
+    if ((rc = upload(&sh->vec, D->vectors, (size_t)D->n * D->d, &sh->bytes))) return fail(rc);
+    if ((rc = upload(&sh->adj, D->adj, (size_t)D->n * D->j, &sh->bytes))) return fail(rc);
+    if ((rc = upload(&sh->gid, D->global_ids, (size_t)D->n, &sh->bytes))) return fail(rc);
+    if (D->direction &&
+        (rc = upload(&sh->dir, D->direction, (size_t)D->n * D->j * sh->W, &sh->bytes)))
+        return fail(rc);
+    if (D->inter_map && (rc = upload(&sh->inter, D->inter_map, (size_t)D->n, &sh->bytes)))
+        return fail(rc);
+    if (D->ghost_n > 0) {
+        sh->gn = D->ghost_n;
+        sh->gj = D->ghost_j;
+        if ((rc = upload(&sh->gids, D->ghost_ids, (size_t)D->ghost_n, &sh->bytes))) return fail(rc);
+        if ((rc = upload(&sh->gadj, D->ghost_adj, (size_t)D->ghost_n * D->ghost_j, &sh->bytes)))
+            return fail(rc);
+        if ((rc = upload(&sh->gvec, nullptr, (size_t)D->ghost_n * D->d, &sh->bytes))) return fail(rc);
+        gather_rows_kernel<<<256, 256>>>(sh->vec, sh->gids, sh->gn, sh->d, sh->gvec);
+        g_launches++;
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return fail(set_err(PW_ECUDA, cudaGetErrorString(e)));
+    }
+    *out = sh;
+    return 0;
+}
+
+int pw_shard_destroy(pw_shard* sh) {
+    if (!sh) return 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(sh->device);
+    void* ptrs[] = {sh->vec, sh->adj, sh->gid, sh->dir, sh->inter, sh->gvec, sh->gadj, sh->gids,
+                    sh->counter, sh->gvis, sh->gscr};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    cudaSetDevice(cur);
+    delete sh;
+    return 0;
+}
+
+int64_t pw_shard_bytes(const pw_shard* sh) { return sh ? sh->bytes : 0; }
+
+int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuning,
+                    const float* queries, int64_t q0, int64_t n, int32_t stage,
+                    const int32_t* entries_in, int32_t* forward_out, int32_t* shard_ids,
+                    float* shard_dists, int32_t n_cols, int32_t col, int32_t* stats_i32,
+                    int64_t* stats_i64, int64_t q_total, void* stream) {
+    if (!sh || !params) return set_err(PW_EINVAL, "null argument");
+    if (forward_out && !sh->inter)
+        return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
+    Launch Lc;
+    bool ghost_on = params->ghost_enabled && !entries_in && sh->gn > 0;
+    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc);
+    if (rc) return rc;
+    KArgs& A = Lc.A;
+    A.stage = stage;
+    A.q0 = q0;
+    A.n_tasks = (int32_t)n;
+    A.queries = queries + q0 * sh->d;
+    A.entries = entries_in ? entries_in + q0 : nullptr;
+    A.forward = forward_out ? forward_out + q0 : nullptr;
+    const int64_t k = params->k;
+    A.out_ids = shard_ids + (q0 * n_cols + col) * k;
+    A.out_dists = shard_dists + (q0 * n_cols + col) * k;
+    A.out_local = nullptr;
+    A.out_stride = (int64_t)n_cols * k;
+    A.st32 = stats_i32 ? stats_i32 + q0 : nullptr;
+    A.st64 = stats_i64 ? stats_i64 + q0 : nullptr;
+    A.st_stride = q_total;
+    return launch(sh, Lc, (cudaStream_t)stream);
+}
+
+int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q, int32_t n_cols,
+                   int32_t k, int32_t* final_ids, float* final_dists, void* stream) {
+    if (q <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int32_t* err = nullptr;
+    PW_CUDA(cudaMallocAsync(&err, sizeof(int32_t), st));
+    PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    const int n = n_cols * k;
+    const int warps = 4;
+    size_t smem = (size_t)warps * n * sizeof(uint64_t);
+    if (smem > 48 * 1024)
+        PW_CUDA(cudaFuncSetAttribute(reduce_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int blocks = (int)std::min<int64_t>(4096, (q + warps - 1) / warps);
+    reduce_topk_kernel<<<blocks, 32 * warps, smem, st>>>(shard_ids, shard_dists, q, n, k, final_ids,
+                                                          final_dists, err);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    int32_t herr = 0;
+    PW_CUDA(cudaMemcpyAsync(&herr, err, sizeof herr, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaFreeAsync(err, st));
+    PW_CUDA(cudaStreamSynchronize(st));
+    if (herr) return set_err(PW_EINVAL, "cannot reduce empty candidate lists");
+    return 0;
+}
+
+int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
+                  const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
+                  int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
+                  int32_t* stats_i32, int64_t* stats_i64, int32_t* entries_a, int32_t* entries_b,
+                  void* stream) {
+    if (N < 1 || !shards) return set_err(PW_EINVAL, "need at least one shard");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t k = params->k;
+    PW_CUDA(cudaMemsetAsync(shard_ids, 0xFF, sizeof(int32_t) * q * N * k, st));  // -1 padding
+    int rc = pw_fill_inf(shard_dists, q * N * k, st);                              // +inf padding
+    if (rc) return rc;
+    PW_CUDA(cudaMemsetAsync(stats_i32, 0, sizeof(int32_t) * 4 * q * N, st));
+    PW_CUDA(cudaMemsetAsync(stats_i64, 0, sizeof(int64_t) * 4 * q * N, st));
+    if (mode == PW_MODE_BASELINE) {
+        for (int s = 0; s < N; s++) {  // pipeline.py:288-297
+            rc = pw_search_stage(shards[s], params, tuning, queries, 0, q, s, nullptr, nullptr,
+                                 shard_ids, shard_dists, N, s, stats_i32 + (int64_t)s * 4 * q,
+                                 stats_i64 + (int64_t)s * 4 * q, q, st);
+            if (rc) return rc;
+        }
+    } else {
+        if (N > 1)
+            for (int s = 0; s < N; s++)
+                if (!shards[s]->inter)
+                    return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
+        std::vector<int64_t> lo(N + 1, 0);  // np.array_split(arange(Q), N)
+        for (int c = 0; c < N; c++) lo[c + 1] = lo[c] + q / N + (c < q % N ? 1 : 0);
+        int32_t* ein = entries_a;
+        int32_t* eout = entries_b;
+        for (int stage = 0; stage < N; stage++) {  // pipeline.py:344-347
+            for (int c = 0; c < N; c++) {
+                int shard = (c + stage) % N;
+                rc = pw_search_stage(shards[shard], params, tuning, queries, lo[c], lo[c + 1] - lo[c],
+                                     stage, stage > 0 ? ein : nullptr,
+                                     stage < N - 1 ? eout : nullptr, shard_ids, shard_dists, N, shard,
+                                     stats_i32 + (int64_t)stage * 4 * q,
+                                     stats_i64 + (int64_t)stage * 4 * q, q, st);
+                if (rc) return rc;
+            }
+            std::swap(ein, eout);
+        }
+    }
+    return 0;
+}
+
+int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw_tuning* tuning,
+           const float* queries, int64_t q, int32_t mode, int32_t* shard_ids, float* shard_dists,
+           int32_t* final_ids, float* final_dists, int32_t* stats_i32, int64_t* stats_i64,
+           int64_t* comm) {
+    if (N < 1 || !shards) return set_err(PW_EINVAL, "need at least one shard");
+    int rc = validate_params(*params);
+    if (rc) return rc;
+    const int64_t k = params->k;
+    const int32_t d = shards[0]->d;
+    cudaStream_t st;
+    PW_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct Bufs {
+        float* q = nullptr;
+        int32_t* sid = nullptr;
+        float* sd = nullptr;
+        int32_t* fid = nullptr;
+        float* fd = nullptr;
+        int32_t* s32 = nullptr;
+        int64_t* s64 = nullptr;
+        int32_t* ea = nullptr;
+        int32_t* eb = nullptr;
+    } B;
+    auto cleanup = [&]() {
+        void* ps[] = {B.q, B.sid, B.sd, B.fid, B.fd, B.s32, B.s64, B.ea, B.eb};
+        for (void* p : ps)
+            if (p) cudaFree(p);
+        cudaStreamDestroy(st);
+    };
+#define PW_TRY(call)                                                                         \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            cleanup();                                                                       \
+            return set_err(e_ == cudaErrorMemoryAllocation ? PW_ENOMEM : PW_ECUDA,           \
+                           std::string(#call) + ": " + cudaGetErrorString(e_));             \
+        }                                                                                    \
+    } while (0)
+    const int64_t qq = std::max<int64_t>(q, 1);
+    PW_TRY(cudaMalloc(&B.q, sizeof(float) * qq * d));
+    PW_TRY(cudaMalloc(&B.sid, sizeof(int32_t) * qq * N * k));
+    PW_TRY(cudaMalloc(&B.sd, sizeof(float) * qq * N * k));
+    PW_TRY(cudaMalloc(&B.fid, sizeof(int32_t) * qq * k));
+    PW_TRY(cudaMalloc(&B.fd, sizeof(float) * qq * k));
+    PW_TRY(cudaMalloc(&B.s32, sizeof(int32_t) * qq * N * 4));
+    PW_TRY(cudaMalloc(&B.s64, sizeof(int64_t) * qq * N * 4));
+    PW_TRY(cudaMalloc(&B.ea, sizeof(int32_t) * qq));
+    PW_TRY(cudaMalloc(&B.eb, sizeof(int32_t) * qq));
+    PW_TRY(cudaMemcpyAsync(B.q, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
+    rc = pw_run_device(shards, N, params, tuning, B.q, q, mode, B.sid, B.sd, B.fid, B.fd, B.s32,
+                       B.s64, B.ea, B.eb, st);
+    if (rc == 0) rc = pw_reduce_topk(B.sid, B.sd, q, N, (int32_t)k, B.fid, B.fd, st);
+    if (rc) {
+        std::string keep = g_err;
+        cleanup();
+        g_err = keep;
+        return rc;
+    }
+    PW_TRY(cudaMemcpyAsync(shard_ids, B.sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
+    PW_TRY(cudaMemcpyAsync(shard_dists, B.sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
+    PW_TRY(cudaMemcpyAsync(final_ids, B.fid, sizeof(int32_t) * q * k, cudaMemcpyDeviceToHost, st));
+    PW_TRY(cudaMemcpyAsync(final_dists, B.fd, sizeof(float) * q * k, cudaMemcpyDeviceToHost, st));
+    PW_TRY(cudaMemcpyAsync(stats_i32, B.s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
+    PW_TRY(cudaMemcpyAsync(stats_i64, B.s64, sizeof(int64_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
+    PW_TRY(cudaStreamSynchronize(st));
+    // comm accounting (pipeline.py:340-341): 4 B per forwarded query
+    std::memset(comm, 0, sizeof(int64_t) * N * N);
+    if (mode == PW_MODE_PIPELINED) {
+        std::vector<int64_t> lo(N + 1, 0);
+        for (int c = 0; c < N; c++) lo[c + 1] = lo[c] + q / N + (c < q % N ? 1 : 0);
+        for (int stage = 0; stage < N - 1; stage++)
+            for (int c = 0; c < N; c++) comm[(int64_t)stage * N + (c + stage) % N] = 4 * (lo[c + 1] - lo[c]);
+    }
+    cleanup();
+#undef PW_TRY
+    return 0;
+}
+
+int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, const float* query,
+                  const int64_t* seeds, int32_t n_seeds, pw_rng* rng, int32_t* out_ids,
+                  float* out_dists, int32_t* out_local, pw_search_out* out, int32_t* visit_log,
+                  int64_t visit_cap) {
+    if (!sh || !params || !rng || !out) return set_err(PW_EINVAL, "null argument");
+    const int64_t n = use_ghost ? sh->gn : sh->n;
+    for (int i = 0; i < n_seeds; i++)  // search.py:215-217
+        if (seeds[i] < 0 || seeds[i] >= n)
+            return set_err(PW_EINVAL, "seed " + std::to_string(seeds[i]) + " outside shard of " +
+                                          std::to_string(n) + " nodes");
+    Launch Lc;
+    int rc = prepare(sh, *params, nullptr, use_ghost != 0, n_seeds, false, Lc);
+    if (rc) return rc;
+    KArgs& A = Lc.A;
+    const int64_t k = params->k;
+    if (!params->log_visits) visit_cap = 0;
+    size_t bytes = 0;
+    auto bump = [&](size_t b) {
+        size_t o = bytes;
+        bytes += (b + 255) / 256 * 256;
+        return o;
+    };
+    size_t o_q = bump(sizeof(float) * sh->d), o_s = bump(sizeof(int64_t) * std::max(n_seeds, 1)),
+           o_r = bump(sizeof(Pcg64)), o_id = bump(sizeof(int32_t) * k), o_d = bump(sizeof(float) * k),
+           o_l = bump(sizeof(int32_t) * k), o_rec = bump(sizeof(TaskRecord)),
+           o_v = bump(sizeof(int32_t) * std::max<int64_t>(visit_cap, 1));
+    char* buf = nullptr;
+    PW_CUDA(cudaSetDevice(sh->device));
+    PW_CUDA(cudaMalloc(&buf, bytes));
+    Pcg64 g{rng->state_hi, rng->state_lo, rng->inc_hi, rng->inc_lo, (uint32_t)rng->has_uint32, rng->uinteger};
+    cudaMemcpy(buf + o_q, query, sizeof(float) * sh->d, cudaMemcpyHostToDevice);
+    if (n_seeds) cudaMemcpy(buf + o_s, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyHostToDevice);
+    cudaMemcpy(buf + o_r, &g, sizeof g, cudaMemcpyHostToDevice);
+    A.stage = 0;
+    A.q0 = 0;
+    A.n_tasks = 1;
+    A.queries = (const float*)(buf + o_q);
+    A.seeds = (const int64_t*)(buf + o_s);
+    A.n_seeds = n_seeds;
+    A.rng_io = (Pcg64*)(buf + o_r);
+    A.out_ids = (int32_t*)(buf + o_id);
+    A.out_dists = (float*)(buf + o_d);
+    A.out_local = (int32_t*)(buf + o_l);
+    A.out_stride = k;
+    A.rec = (TaskRecord*)(buf + o_rec);
+    A.visit_log = visit_cap ? (int32_t*)(buf + o_v) : nullptr;
+    A.visit_cap = visit_cap;
+    rc = launch(sh, Lc, 0);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (!rc && e != cudaSuccess) rc = set_err(PW_ECUDA, cudaGetErrorString(e));
+    if (!rc) {
+        TaskRecord R;
+        cudaMemcpy(&R, buf + o_rec, sizeof R, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&g, buf + o_r, sizeof g, cudaMemcpyDeviceToHost);
+        cudaMemcpy(out_ids, buf + o_id, sizeof(int32_t) * R.n_out, cudaMemcpyDeviceToHost);
+        cudaMemcpy(out_dists, buf + o_d, sizeof(float) * R.n_out, cudaMemcpyDeviceToHost);
+        if (out_local) cudaMemcpy(out_local, buf + o_l, sizeof(int32_t) * R.n_out, cudaMemcpyDeviceToHost);
+        if (visit_cap && visit_log)
+            cudaMemcpy(visit_log, buf + o_v, sizeof(int32_t) * std::min<int64_t>(R.n_visited, visit_cap),
+                       cudaMemcpyDeviceToHost);
+        out->iterations = R.c[0];
+        out->distance_computations = R.c[1];
+        out->total_visits = R.c[2];
+        out->nodes_expanded = R.c[3];
+        out->dgs_skipped = R.c[4];
+        out->inserted_total = R.c[5];
+        out->converged = R.converged;
+        out->retained = R.retained;
+        out->n_out = R.n_out;
+        out->n_visited = R.n_visited;
+        rng->state_hi = g.s_hi;
+        rng->state_lo = g.s_lo;
+        rng->inc_hi = g.i_hi;
+        rng->inc_lo = g.i_lo;
+        rng->has_uint32 = (int32_t)g.has32;
+        rng->uinteger = g.u32;
+    }
+    cudaFree(buf);
+    return rc;
+}
+
+int pw_squared_l2_rows(pw_shard* sh, const int32_t* ids, int64_t n_ids, const float* query,
+                       float* out, void* stream) {
+    if (!sh) return set_err(PW_EINVAL, "null argument");
+    if (n_ids <= 0) return 0;
+    L2Plan plan;
+    if (!make_plan(sh->d, plan)) return set_err(PW_EINVAL, "dimension too large");
+    int spad = (sh->d + 31) / 32 * 32 + 8;
+    if (spad - 32 >= sh->d) spad -= 32;
+    size_t smem = sizeof(float) * (((sh->d + 3) & ~3) + 4 * spad);
+    if (smem > 48 * 1024)
+        PW_CUDA(cudaFuncSetAttribute(l2_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int blocks = (int)std::min<int64_t>(4096, (n_ids + 3) / 4);
+    l2_rows_kernel<<<blocks, 32, smem, (cudaStream_t)stream>>>(sh->vec, sh->d, spad, plan, ids, n_ids,
+                                                               query, out);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void fill_kernel(float* p, int64_t n, float v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+int pw_fill_inf(float* p, int64_t n, cudaStream_t st) {
+    if (n <= 0) return 0;
+    fill_kernel<<<(int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, st>>>(p, n, INFINITY);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
+}
+}  // namespace

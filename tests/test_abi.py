@@ -1,0 +1,67 @@
+"""The C-ABI library loads and exports every symbol include/pw_b200.h declares
+(no compute calls: runs without a GPU)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def declared_functions():
+    text = (ROOT / "include" / "pw_b200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w]+\s*\*?\s*(pw_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_entry_points():
+    names = declared_functions()
+    for must in ("pw_shard_create", "pw_search_one", "pw_search_stage", "pw_run", "pw_reduce_topk"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2507_17094_b200 import _abi
+
+    assert _abi.LIB_PATH.exists(), "libpwb200.so not built (run __graft_entry__.build())"
+    lib = ctypes.CDLL(str(_abi.LIB_PATH))
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert set(declared_functions()) == set(_abi.EXPORTS)
+
+
+def test_version_string():
+    from paper_2507_17094_b200 import _abi
+
+    lib = _abi.load(require_device=False)
+    assert b"sm_100a" in lib.pw_version()
+
+
+def test_sass_is_sm100a():
+    import shutil
+    import subprocess
+
+    from paper_2507_17094_b200 import _abi
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not on PATH")
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_abi.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("device present")
+    import numpy as np
+
+    import paper_2507_17094_b200 as pw
+    from paper_2507_17094_b200.rng import stream
+
+    ctx = pw.ShardContext(vectors=np.zeros((4, 2), np.float32), adj=np.zeros((4, 1), np.int32),
+                          global_ids=np.arange(4, dtype=np.int32))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        pw.search(np.zeros(2, np.float32), ctx, pw.SearchParams(k=1, l=4, m=4, r=1), rng=stream(0, 4, 0, 0))

@@ -1,0 +1,263 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+* golden fixtures produced by the reference itself (tests/golden/): every
+  array of every PipelineResult bit-equal, every counter equal;
+* the CPU oracle (pinned to the same goldens) at sizes/dims the fixtures do
+  not cover (d = 96 / 128 / 200 / 960, 2-4 shards, thousands of queries).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2507_17094_b200 as pw
+from golden_util import (GOLDEN, assert_run_equal, expected, load, oracle_dict, result_dict,
+                         sift_cases, small_cases)
+from paper_2507_17094_b200.rng import TAG_SEARCH, stream
+from paper_2507_17094_b200.search import SearchParams, ShardContext
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def small():
+    z, base, queries, index, ctxs = load("small")
+    return z, base, pw.Dataset(queries), index, pw.build_contexts(index, base)
+
+
+@pytest.fixture(scope="module")
+def sift():
+    z, base, queries, index, ctxs = load("sift128")
+    return z, base, pw.Dataset(queries), index, pw.build_contexts(index, base)
+
+
+@pytest.mark.parametrize("case", small_cases(), ids=lambda c: c[0])
+def test_small_golden(small, case):
+    name, params, mode, prefix = case
+    z, base, queries, index, ctxs = small
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(queries, index, base, params, contexts=ctxs))
+    assert_run_equal(got, expected(z, prefix), name)
+
+
+@pytest.mark.parametrize("case", sift_cases(), ids=lambda c: c[0])
+def test_sift128_golden(sift, case):
+    name, params, mode, prefix = case
+    z, base, queries, index, ctxs = sift
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(queries, index, base, params, contexts=ctxs))
+    assert_run_equal(got, expected(z, prefix), name)
+
+
+def test_build_contexts_from_index(small):
+    z, base, queries, index, _ = small
+    params = SearchParams(k=10, l=32, m=32, r=4, max_iter=24, seed=17, cooldown_ratio=0.3,
+                          ghost_max_iter=6)
+    got = result_dict(pw.run_pipelined(queries, index, base, params))
+    assert_run_equal(got, expected(z, "arm00_pipelined_"), "contexts=None")
+
+
+@pytest.mark.parametrize("d", [1, 2, 7, 16, 32, 96, 128, 200, 960])
+def test_squared_l2_primitive_golden(d):
+    import torch
+
+    z = np.load(GOLDEN / "l2.npz")
+    x, q = z[f"x{d}"], z[f"q{d}"]
+    ctx = ShardContext(vectors=x, adj=np.zeros((x.shape[0], 0), np.int32),
+                       global_ids=np.arange(x.shape[0], dtype=np.int32))
+    dev = pw.device_shard(ctx)
+    lib = pw._abi.load()
+    ids = torch.arange(x.shape[0], dtype=torch.int32, device="cuda")
+    tq = torch.from_numpy(q).cuda()
+    out = torch.empty(x.shape[0], dtype=torch.float32, device="cuda")
+    pw._abi.check(lib.pw_squared_l2_rows(dev.handle, ids.data_ptr(), x.shape[0], tq.data_ptr(),
+                                         out.data_ptr(), None))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), z[f"sq{d}"])
+
+
+def _ctx(vectors, adj):
+    return ShardContext(vectors=vectors, adj=adj, global_ids=np.arange(vectors.shape[0], dtype=np.int32))
+
+
+def test_search_complete_graph_exact():
+    """reference tests/test_search.py:105-115 (ids AND dists bit-equal)."""
+    z = np.load(GOLDEN / "search.npz")
+    ctx = _ctx(z["complete_vectors"], z["complete_adj"])
+    params = SearchParams(k=10, l=16, m=8, r=2, max_iter=20, seed=5)
+    for qi in range(10):
+        q = ctx.vectors[qi] + np.float32(0.01)
+        res = pw.search(q, ctx, params, seeds=(0,), rng=stream(5, TAG_SEARCH, qi, 0))
+        assert res.ids.tolist() == z["complete_ids"][qi].tolist()
+        assert np.array_equal(res.dists, z["complete_dists"][qi])
+        assert res.converged
+
+
+def test_search_buffer_cap_visit_order():
+    """reference tests/test_search.py:197-205."""
+    z = np.load(GOLDEN / "search.npz")
+    ctx = _ctx(np.arange(10, dtype=np.float32)[:, None], z["line_adj"])
+    params = SearchParams(k=1, l=4, m=1, r=1, max_iter=2, seed=0, buffer_cap=5, log_visits=True)
+    res = pw.search(np.zeros(1, np.float32), ctx, params, seeds=(9,), rng=stream(0, TAG_SEARCH, 0, 0))
+    assert res.visited_ids.tolist() == z["line_visited"].tolist()
+    assert res.counters.total_visits == int(z["line_total_visits"])
+
+
+def test_search_visit_log_counters_and_rng_state():
+    """log_visits order, all counters, and the caller's Generator advanced like numpy."""
+    z = np.load(GOLDEN / "search.npz")
+    ctx = _ctx(z["visit_vectors"], z["visit_adj"])
+    params = SearchParams(k=5, l=16, m=16, r=4, max_iter=12, seed=2, log_visits=True)
+    g = stream(2, TAG_SEARCH, 3, 0)
+    res = pw.search(ctx.vectors[3], ctx, params, rng=g)
+    assert res.visited_ids.tolist() == z["visit_log"].tolist()
+    assert res.ids.tolist() == z["visit_ids"].tolist()
+    assert np.array_equal(res.dists, z["visit_dists"])
+    c = res.counters
+    assert [c.iterations, c.distance_computations, c.total_visits, c.nodes_expanded,
+            c.dgs_skipped, c.inserted_total] == z["visit_counters"].tolist()
+    st = g.bit_generator.state
+    after = z["visit_rng_after"]
+    assert st["state"]["state"] == (int(after[0]) << 64) | int(after[1])
+    assert st["has_uint32"] == int(after[2]) and st["uinteger"] == int(after[3])
+
+
+def test_single_node_graph():
+    """reference tests/test_search.py:118-128 (degree-0 graph)."""
+    ctx = ShardContext(vectors=np.array([[1.0, 2.0]], dtype=np.float32),
+                       adj=np.empty((1, 0), dtype=np.int32), global_ids=np.array([7], dtype=np.int32))
+    params = SearchParams(k=1, l=4, m=4, r=1, max_iter=8, seed=0)
+    res = pw.search(np.array([1.0, 0.0]), ctx, params, rng=stream(0, TAG_SEARCH, 0, 0))
+    assert res.ids.tolist() == [7]
+    assert res.dists[0] == pytest.approx(2.0)
+    assert res.converged
+
+
+def test_search_matches_oracle_all_selections(small):
+    z, base, queries, index, ctxs = small
+    ctx = ctxs[1]
+    for sel, dr in (("full", 0.0), ("direction", 0.5), ("random", 0.5)):
+        params = SearchParams(k=10, l=32, m=32, r=4, max_iter=16, seed=9, selection=sel,
+                              discard_ratio=dr, cooldown_ratio=0.25, log_visits=True)
+        for qi in range(0, 100, 9):
+            q = queries.data[qi]
+            g = stream(9, TAG_SEARCH, qi, 1)
+            res = pw.search(q, ctx, params, rng=g)
+            want, st = oracle.search(q, ctx, params, rng_state=oracle.pcg64_state(
+                pw.rng.derive_seed(9, TAG_SEARCH, qi, 1)))
+            assert res.ids.tolist() == want["ids"].tolist()
+            assert np.array_equal(res.dists, want["dists"])
+            assert res.visited_ids.tolist() == want["visited_ids"].tolist()
+            assert res.counters.__dict__ == want["counters"]
+            assert g.bit_generator.state["state"] == st["state"]
+
+
+def test_ghost_stage_matches_oracle(small):
+    z, base, queries, index, ctxs = small
+    params = SearchParams(k=10, l=32, m=32, r=4, max_iter=24, seed=17, ghost_enabled=True,
+                          ghost_max_iter=6)
+    for s, ctx in enumerate(ctxs):
+        for qi in range(0, 100, 13):
+            g = stream(17, 5, qi, s)
+            entry, counters = pw.run_ghost_stage(queries.data[qi], ctx, params, rng=g)
+            e2, c2, _ = oracle.ghost_stage(queries.data[qi], ctx, params, rng_state=oracle.pcg64_state(
+                pw.rng.derive_seed(17, 5, qi, s)))
+            assert entry == e2
+            assert counters.iterations == c2["iterations"]
+            assert counters.distance_computations == c2["distance_computations"]
+
+
+def test_ghost_stage_identity_with_full_sample(small):
+    """reference tests/test_pipeline.py:137-159 with ghost graph == main graph."""
+    z, base, queries, index, ctxs = small
+    v = ctxs[0].vectors[:500]
+    from index_util import knn_graph
+    adj = knn_graph(v, 8)
+    ids = np.arange(500, dtype=np.int32)
+    ctx = ShardContext(vectors=v, adj=adj, global_ids=ids,
+                       ghost=pw.GhostContext(vectors=v, adj=adj, parent_ids=ids))
+    params = SearchParams(k=1, l=16, m=16, r=4, max_iter=6, seed=5, ghost_enabled=True,
+                          ghost_max_iter=6)
+    for qi in range(5):
+        q = queries.data[qi]
+        entry, counters = pw.run_ghost_stage(q, ctx, params, rng=stream(5, TAG_SEARCH, qi, 0))
+        res = pw.search(q, ctx, params.with_(k=1, ghost_enabled=False),
+                        rng=stream(5, TAG_SEARCH, qi, 0), query_id=qi)
+        assert entry == res.local_ids[0]
+        assert counters.iterations <= params.ghost_max_iter
+
+
+def test_reduce_topk_goldens():
+    """reference tests/test_pipeline.py:48-69."""
+    ids, dists = pw.reduce_topk(np.array([5, 9, 1]), np.array([0.5, 0.1, 0.9], np.float32), 2)
+    assert ids.tolist() == [9, 5]
+    ids, dists = pw.reduce_topk(np.array([3, 2, -1, 7]), np.array([0.5, 0.5, np.inf, 0.25], np.float32), 3)
+    assert ids.tolist() == [7, 2, 3]
+    with pytest.raises(ValueError, match="empty"):
+        pw.reduce_topk(np.array([-1, -1]), np.array([np.inf, np.inf], np.float32), 2)
+
+
+def test_validation_errors(small):
+    z, base, queries, index, ctxs = small
+    params = SearchParams(k=1, l=4, m=4, r=1, max_iter=4, seed=0)
+    line = _ctx(np.arange(10, dtype=np.float32)[:, None], np.zeros((10, 2), np.int32))
+    with pytest.raises(ValueError, match="seed"):
+        pw.search(np.zeros(1, np.float32), line, params, seeds=(99,), rng=stream(0, 4, 0, 0))
+    with pytest.raises(ValueError, match="does not match"):
+        pw.search(np.zeros(3, np.float32), line, params, rng=stream(0, 4, 0, 0))
+    with pytest.raises(ValueError, match="direction table"):
+        pw.search(np.zeros(1, np.float32), line, params.with_(selection="direction", discard_ratio=0.5),
+                  rng=stream(0, 4, 0, 0))
+    with pytest.raises(ValueError, match="ghost"):
+        pw.run_ghost_stage(np.zeros(1, np.float32), line, params.with_(ghost_enabled=True),
+                           rng=stream(0, 4, 0, 0))
+    stripped = pw.Index(d=index.d, n_total=index.n_total,
+                        shards=[pw.ShardPack(p.global_ids, p.adj, None, None, None, None)
+                                for p in index.shards])
+    with pytest.raises(ValueError, match="inter-shard"):
+        pw.run_pipelined(queries, stripped, base, params)
+    with pytest.raises(ValueError, match="does not match"):
+        pw.build_contexts(index, pw.Dataset(np.zeros((base.n, base.d + 1), np.float32)))
+
+
+@pytest.fixture(scope="module")
+def synth():
+    from index_util import clustered, make_contexts
+    out = {}
+    for d, n, nq, shards, j in ((96, 24000, 600, 2, 32), (128, 12000, 300, 3, 32),
+                                (200, 6000, 200, 2, 24), (960, 3000, 64, 2, 32)):
+        x = clustered(n + nq, d, 512, 0.08, seed=d)
+        out[d] = (np.ascontiguousarray(x[n:]), make_contexts(x[:n], shards, j, seed=d))
+    return out
+
+
+SYNTH_ARMS = [
+    dict(k=10, l=64, m=64, r=8, max_iter=64, seed=1),
+    dict(k=10, l=128, m=64, r=8, max_iter=64, seed=2, selection="direction", discard_ratio=0.5,
+         cooldown_ratio=0.3, ghost_enabled=True, ghost_max_iter=8),
+    dict(k=10, l=96, m=64, r=4, max_iter=10, seed=3, selection="random", discard_ratio=0.5,
+         seed_mode="mixed", ghost_enabled=True),
+    dict(k=16, l=256, m=128, r=16, max_iter=64, seed=4),
+]
+
+
+@pytest.mark.parametrize("d", [96, 128, 200, 960])
+@pytest.mark.parametrize("arm", range(len(SYNTH_ARMS)))
+@pytest.mark.parametrize("mode", ["baseline", "pipelined"])
+def test_synthetic_matches_oracle(synth, d, arm, mode):
+    queries, ctxs = synth[d]
+    params = SearchParams(**SYNTH_ARMS[arm])
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(pw.Dataset(queries), None, None, params, contexts=ctxs))
+    want = oracle_dict(oracle.run(queries, ctxs, params, mode))
+    assert_run_equal(got, want, f"d={d} arm={arm} {mode}")
+
+
+def test_visited_spill_to_global_table(synth):
+    """Tiny shared-memory visited table forces the exact global spill path."""
+    queries, ctxs = synth[96]
+    params = SearchParams(**SYNTH_ARMS[3])
+    got = result_dict(pw.run_sharded_baseline(pw.Dataset(queries), None, None, params, contexts=ctxs,
+                                              tuning={"visited_slots": 256}))
+    want = oracle_dict(oracle.run(queries, ctxs, params, "baseline"))
+    assert_run_equal(got, want, "spill")
