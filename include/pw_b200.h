@@ -132,11 +132,12 @@ int pw_search_stage(pw_shard* shard, const pw_params* params, const pw_tuning* t
                     int32_t* stats_i32, int64_t* stats_i64, int64_t q_total, void* stream);
 
 /* pipeline.py:187-196 reduce_topk + :249-267 finish over device arrays:
- * (q, n_cols, k) -> (q, k), by (sqrt'd float32 distance, global id).
+ * (q, n_cand) candidate lists (n_cand = N*k for (q, N, k) shard lists) ->
+ * (q, k) by (sqrt'd float32 distance, global id); ids < 0 are padding.
  * Returns PW_EINVAL "cannot reduce empty candidate lists" if some query has
  * no valid candidate. */
 int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q,
-                   int32_t n_cols, int32_t k, int32_t* final_ids, float* final_dists,
+                   int32_t n_cand, int32_t k, int32_t* final_ids, float* final_dists,
                    void* stream);
 
 /* Replaces pipeline.py:270-305 run_sharded_baseline (mode 0) and

@@ -215,22 +215,25 @@ struct WarpState {
 __device__ __forceinline__ uint32_t bh_insert(const KArgs& A, WarpState& S, uint32_t id) {
     const uint32_t mask = (uint32_t)A.BH - 1u;
     uint32_t h = hash32(id) & mask;
-    while (true) {
+    for (int probe = 0; probe <= A.BH; probe++) {
         uint32_t old = atomicCAS(&S.bhk[h], kEmpty, id);
         if (old == kEmpty || old == id) return h;
         h = (h + 1u) & mask;
     }
+    atomicOr(A.err, 2);  // batch table full: impossible when BH >= 2*CB
+    return h;
 }
 
 __device__ __forceinline__ bool bh_contains(const KArgs& A, const WarpState& S, uint32_t id) {
     const uint32_t mask = (uint32_t)A.BH - 1u;
     uint32_t h = hash32(id) & mask;
-    while (true) {
+    for (int probe = 0; probe <= A.BH; probe++) {
         uint32_t v = S.bhk[h];
         if (v == id) return true;
         if (v == kEmpty) return false;
         h = (h + 1u) & mask;
     }
+    return false;
 }
 
 __device__ __forceinline__ void bh_clear(const KArgs& A, WarpState& S) {
@@ -271,28 +274,33 @@ __device__ int dedup_ordered(const KArgs& A, WarpState& S, const int32_t* src, i
 __device__ __forceinline__ bool visit_insert(const KArgs& A, WarpState& S, uint32_t id) {
     const uint32_t hm = (uint32_t)A.H - 1u;
     uint32_t h = hash32(id) & hm;
-    while (true) {
+    int probe = 0;
+    for (; probe <= A.H; probe++) {
         uint32_t v = S.vh[h];
         if (v == id) return false;
         if (v == kEmpty) break;
         h = (h + 1u) & hm;
     }
     if (!S.ovf) {
-        while (true) {
+        for (; probe <= A.H; probe++) {
             uint32_t old = atomicCAS(&S.vh[h], kEmpty, id);
             if (old == kEmpty) return true;
             if (old == id) return false;
             h = (h + 1u) & hm;
         }
+        atomicOr(A.err, 4);  // smem visited table full: impossible below vis_limit
+        return false;
     }
     const uint32_t gm = (uint32_t)A.gmask;
     uint32_t g = (hash32(id ^ 0x5bd1e995u) >> 3) & gm;
-    while (true) {
+    for (uint32_t gp = 0; gp <= gm; gp++) {
         uint32_t old = atomicCAS(&S.gvis[g], kEmpty, id);
         if (old == kEmpty) return true;
         if (old == id) return false;
         g = (g + 1u) & gm;
     }
+    atomicOr(A.err, 8);  // global visited table full
+    return false;
 }
 
 // Keep only never-scored ids of newl[0..nb) (in order); returns n_new.

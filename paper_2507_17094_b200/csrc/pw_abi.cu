@@ -349,12 +349,17 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
 
     // ---- global workspace: visited spill tables + choice scratch
     const int total_warps = Lc.blocks * wpb;
-    int64_t gsz = bound > A.vis_limit ? next_pow2(2 * bound + 2) : 1;
+    // the spill triggers when (smem entries + batch) > vis_limit, so a table is
+    // needed whenever bound + CB can exceed it; it holds <= bound entries
+    int64_t gsz = bound + cb > A.vis_limit ? next_pow2(2 * bound + 2) : 1;
     A.gmask = (int32_t)(gsz - 1);
     int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
     int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
     std::lock_guard<std::mutex> lk(sh->mu);
-    if (!sh->counter) PW_CUDA(cudaMalloc(&sh->counter, sizeof(int32_t) * 2));
+    if (!sh->counter) {
+        PW_CUDA(cudaMalloc(&sh->counter, sizeof(int32_t) * 2));
+        PW_CUDA(cudaMemset(sh->counter, 0, sizeof(int32_t) * 2));
+    }
     if (sh->gvis_words < (size_t)total_warps * gsz) {
         if (sh->gvis) cudaFree(sh->gvis);
         sh->gvis = nullptr;
@@ -375,10 +380,21 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     return 0;
 }
 
+// Device-side consistency flag (bounded probes in K1); read after a sync.
+int check_err(pw_shard* sh) {
+    int32_t e = 0;
+    PW_CUDA(cudaMemcpy(&e, sh->counter + 1, sizeof e, cudaMemcpyDeviceToHost));
+    if (e) {
+        cudaMemset(sh->counter + 1, 0, sizeof(int32_t));
+        return set_err(PW_ECUDA, "beam_search_kernel internal table overflow (flag " + std::to_string(e) + ")");
+    }
+    return 0;
+}
+
 int launch(pw_shard* sh, Launch& Lc, cudaStream_t st) {
     if (Lc.A.n_tasks <= 0) return 0;
     PW_CUDA(cudaSetDevice(sh->device));
-    PW_CUDA(cudaMemsetAsync(sh->counter, 0, sizeof(int32_t), st));
+    PW_CUDA(cudaMemsetAsync(sh->counter, 0, sizeof(int32_t), st));  // task counter only; err sticks
     int blocks = std::min<int64_t>(Lc.blocks, ((int64_t)Lc.A.n_tasks + Lc.warps_per_block - 1) / Lc.warps_per_block);
     beam_search_kernel<<<blocks, 32 * Lc.warps_per_block, Lc.smem, st>>>(Lc.A);
     g_launches++;
@@ -484,14 +500,14 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
     return launch(sh, Lc, (cudaStream_t)stream);
 }
 
-int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q, int32_t n_cols,
+int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q, int32_t n_cand,
                    int32_t k, int32_t* final_ids, float* final_dists, void* stream) {
     if (q <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     int32_t* err = nullptr;
     PW_CUDA(cudaMallocAsync(&err, sizeof(int32_t), st));
     PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
-    const int n = n_cols * k;
+    const int n = n_cand;
     const int warps = 4;
     size_t smem = (size_t)warps * n * sizeof(uint64_t);
     if (smem > 48 * 1024)
@@ -604,7 +620,7 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     PW_TRY(cudaMemcpyAsync(B.q, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
     rc = pw_run_device(shards, N, params, tuning, B.q, q, mode, B.sid, B.sd, B.fid, B.fd, B.s32,
                        B.s64, B.ea, B.eb, st);
-    if (rc == 0) rc = pw_reduce_topk(B.sid, B.sd, q, N, (int32_t)k, B.fid, B.fd, st);
+    if (rc == 0) rc = pw_reduce_topk(B.sid, B.sd, q, (int32_t)(N * k), (int32_t)k, B.fid, B.fd, st);
     if (rc) {
         std::string keep = g_err;
         cleanup();
@@ -618,6 +634,13 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     PW_TRY(cudaMemcpyAsync(stats_i32, B.s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
     PW_TRY(cudaMemcpyAsync(stats_i64, B.s64, sizeof(int64_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
     PW_TRY(cudaStreamSynchronize(st));
+    for (int s = 0; s < N; s++)
+        if ((rc = check_err(shards[s]))) {
+            std::string keep = g_err;
+            cleanup();
+            g_err = keep;
+            return rc;
+        }
     // comm accounting (pipeline.py:340-341): 4 B per forwarded query
     std::memset(comm, 0, sizeof(int64_t) * N * N);
     if (mode == PW_MODE_PIPELINED) {
@@ -681,6 +704,7 @@ int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, cons
     rc = launch(sh, Lc, 0);
     cudaError_t e = cudaDeviceSynchronize();
     if (!rc && e != cudaSuccess) rc = set_err(PW_ECUDA, cudaGetErrorString(e));
+    if (!rc) rc = check_err(sh);
     if (!rc) {
         TaskRecord R;
         cudaMemcpy(&R, buf + o_rec, sizeof R, cudaMemcpyDeviceToHost);

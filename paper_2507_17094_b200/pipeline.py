@@ -163,7 +163,7 @@ def reduce_topk(ids: np.ndarray, dists: np.ndarray, k: int):
     oi = torch.empty(k, dtype=torch.int32, device=dev)
     od = torch.empty(k, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
-    _abi.check(lib.pw_reduce_topk(ti.data_ptr(), td.data_ptr(), 1, ids.size, 1, oi.data_ptr(),
+    _abi.check(lib.pw_reduce_topk(ti.data_ptr(), td.data_ptr(), 1, ids.size, k, oi.data_ptr(),
                                   od.data_ptr(), stream))
     oi, od = oi.cpu().numpy(), od.cpu().numpy()
     n = int((oi >= 0).sum())
