@@ -74,6 +74,7 @@ typedef struct {
     int32_t ghost_j;
     const int32_t* ghost_ids;     /* (ghost_n,) parent-local ids, sorted */
     const int32_t* ghost_adj;     /* (ghost_n, ghost_j) ghost-local ids */
+    int32_t on_device;            /* 1: every pointer above is a device pointer (copied D2D) */
 } pw_shard_desc;
 
 typedef struct pw_shard pw_shard;
@@ -122,7 +123,9 @@ int pw_search_one(pw_shard* shard, int32_t use_ghost, const pw_params* params,
  *   forward_out  (q_total,) int32 <- inter_map[top1], or NULL (last stage)
  *   shard_ids/shard_dists (q_total, n_cols, k) written at column `col`
  *   stats_i32 (4, q_total): iterations, ghost_iterations, retained, converged
- *   stats_i64 (4, q_total): distance_computations, total_visits, inserted, dgs_skipped
+ *   stats_i64 (6, q_total): distance_computations, total_visits, inserted, dgs_skipped,
+ *                           nodes_expanded, ghost_nodes_expanded (the last two are not
+ *                           StageStats fields; they feed the gather-roofline byte count)
  * Counters accumulate (+=) like pipeline.py:224-243; converged is assigned.
  * stream: cudaStream_t (NULL = legacy default stream). */
 int pw_search_stage(pw_shard* shard, const pw_params* params, const pw_tuning* tuning,
@@ -134,25 +137,27 @@ int pw_search_stage(pw_shard* shard, const pw_params* params, const pw_tuning* t
 /* pipeline.py:187-196 reduce_topk + :249-267 finish over device arrays:
  * (q, n_cand) candidate lists (n_cand = N*k for (q, N, k) shard lists) ->
  * (q, k) by (sqrt'd float32 distance, global id); ids < 0 are padding.
- * Returns PW_EINVAL "cannot reduce empty candidate lists" if some query has
- * no valid candidate. */
+ * err_dev: device int32 flag set to 1 when some query has no valid candidate;
+ * NULL = synchronise and return PW_EINVAL "cannot reduce empty candidate lists". */
 int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q,
                    int32_t n_cand, int32_t k, int32_t* final_ids, float* final_dists,
-                   void* stream);
+                   int32_t* err_dev, void* stream);
 
 /* Replaces pipeline.py:270-305 run_sharded_baseline (mode 0) and
  * :308-350 run_pipelined (mode 1) for n_shards shards resident on the
  * current device (logical shards; the multi-GPU ring lives in the host
  * layer).  HOST buffers in and out: queries (q, d); shard_ids/dists (q, N, k);
- * final_ids/dists (q, k); stats_i32/i64 (N, 4, q) as in pw_search_stage;
+ * final_ids/dists (q, k); stats_i32 (N, 4, q) / stats_i64 (N, 6, q) as in
+ * pw_search_stage;
  * comm (N, N) int64 bytes per (stage, sending shard). */
 int pw_run(pw_shard* const* shards, int32_t n_shards, const pw_params* params,
            const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
            int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
            int32_t* stats_i32, int64_t* stats_i64, int64_t* comm);
 
-/* Kernel-only timing hook used by bench.py: device-resident variant of
- * pw_run (all pointers device; no host copies, no synchronisation). */
+/* Device-resident variant of pw_run (all pointers device; stats_i64 is
+ * (N, 6, q); no host copies, no synchronisation): the kernel-only timing
+ * path of bench.py. */
 int pw_run_device(pw_shard* const* shards, int32_t n_shards, const pw_params* params,
                   const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
                   int32_t* shard_ids, float* shard_dists, int32_t* final_ids,

@@ -40,6 +40,7 @@ class ShardDesc(C.Structure):
         ("vectors", C.c_void_p), ("adj", C.c_void_p), ("global_ids", C.c_void_p),
         ("direction", C.c_void_p), ("inter_map", C.c_void_p), ("ghost_n", C.c_int64),
         ("ghost_j", C.c_int32), ("ghost_ids", C.c_void_p), ("ghost_adj", C.c_void_p),
+        ("on_device", C.c_int32),
     ]
 
 
@@ -72,7 +73,7 @@ EXPORTS = {
                                   C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_int64, C.c_void_p]),
     "pw_reduce_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
-                                 C.c_void_p, C.c_void_p, C.c_void_p]),
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pw_run": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Params), C.POINTER(Tuning), C.c_void_p,
                          C.c_int64, C.c_int32] + [C.c_void_p] * 7),
     "pw_run_device": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Params), C.POINTER(Tuning),

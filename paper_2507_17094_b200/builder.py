@@ -56,6 +56,26 @@ def gen_clustered(n: int, d: int, n_clusters: int, spread: float, seed: int,
     return out
 
 
+def gen_latent(n: int, d: int, m: int, n_clusters: int, spread: float, noise: float, seed: int,
+               device="cuda") -> torch.Tensor:
+    """Low-intrinsic-dimension variant of the same clustered-Gaussian family:
+    latent z = centre[i % n_clusters] + spread * N(0, I_m) in [0,1]^m, lifted to
+    d dims by a fixed random linear map, plus isotropic noise.  Real descriptor
+    sets (DEEP, SIFT) have intrinsic dimension far below d; this keeps graph
+    navigation realistic at 10M points."""
+    g = _gen(seed, device)
+    centres = torch.rand((n_clusters, m), generator=g, device=device, dtype=torch.float32)
+    lift = torch.randn((m, d), generator=g, device=device, dtype=torch.float32) / math.sqrt(m)
+    out = torch.empty((n, d), device=device, dtype=torch.float32)
+    step = 1 << 22
+    for lo in range(0, n, step):
+        hi = min(n, lo + step)
+        idx = torch.arange(lo, hi, device=device) % n_clusters
+        z = centres[idx] + spread * torch.randn((hi - lo, m), generator=g, device=device)
+        out[lo:hi] = z @ lift + noise * torch.randn((hi - lo, d), generator=g, device=device)
+    return out
+
+
 def partition(n: int, n_shards: int, seed: int, device="cuda") -> list[torch.Tensor]:
     perm = torch.randperm(n, generator=_gen(seed + 0x51, device), device=device)
     return [torch.sort(perm[s::n_shards]).values for s in range(n_shards)]
@@ -82,12 +102,38 @@ def kmeans(x: torch.Tensor, n_lists: int, iters: int, seed: int) -> tuple[torch.
     cent = x[pick].clone()
     assign = _nearest_centroid(x, cent)
     for _ in range(iters):
-        sums = torch.zeros_like(cent).index_add_(0, assign, x)
-        cnt = torch.bincount(assign, minlength=n_lists).to(x.dtype)
+        sums = _segment_sums(x, assign, n_lists)
+        cnt = torch.bincount(assign, minlength=n_lists).to(torch.float64)
         keep = cnt > 0
-        cent[keep] = sums[keep] / cnt[keep, None]
+        cent[keep] = (sums[keep] / cnt[keep, None]).to(cent.dtype)
         assign = _nearest_centroid(x, cent)
     return cent, assign
+
+
+def _segment_sums(x: torch.Tensor, seg: torch.Tensor, n_seg: int) -> torch.Tensor:
+    """Deterministic per-segment float64 sums: stable sort by segment, running
+    float64 prefix sums, differences at segment ends (index_add_ uses atomics
+    whose order, and therefore rounding, varies run to run)."""
+    order = torch.sort(seg, stable=True).indices
+    counts = torch.bincount(seg, minlength=n_seg)
+    ends = torch.cumsum(counts, 0)                        # exclusive end of each segment
+    at_end = torch.zeros((n_seg, x.shape[1]), dtype=torch.float64, device=x.device)
+    carry = torch.zeros(x.shape[1], dtype=torch.float64, device=x.device)
+    step = 1 << 21
+    for lo in range(0, x.shape[0], step):
+        hi = min(lo + step, x.shape[0])
+        cs = torch.cumsum(x[order[lo:hi]].double(), 0) + carry
+        carry = cs[-1]
+        sel = (ends >= lo + 1) & (ends <= hi) & (counts > 0)
+        at_end[sel] = cs[ends[sel] - 1 - lo]
+    # prefix value at the end of the previous non-empty segment
+    idx = torch.where(counts > 0, torch.arange(n_seg, device=x.device),
+                      torch.full((n_seg,), -1, device=x.device, dtype=torch.int64))
+    last = torch.cummax(idx, 0).values
+    prefix = torch.where(last[:, None] >= 0, at_end[last.clamp(min=0)], torch.zeros_like(at_end))
+    prev = torch.zeros_like(prefix)
+    prev[1:] = prefix[:-1]
+    return torch.where((counts > 0)[:, None], prefix - prev, torch.zeros_like(prefix))
 
 
 class IVF:
@@ -96,7 +142,7 @@ class IVF:
     def __init__(self, base: torch.Tensor, n_lists: int, iters: int = 2, seed: int = 0):
         self.base = base
         self.cent, assign = kmeans(base, n_lists, iters, seed)
-        self.order = torch.argsort(assign)
+        self.order = torch.sort(assign, stable=True).indices
         counts = torch.bincount(assign, minlength=self.cent.shape[0])
         self.offsets = torch.zeros(counts.numel() + 1, dtype=torch.int64, device=base.device)
         self.offsets[1:] = torch.cumsum(counts, 0)
@@ -117,7 +163,7 @@ class IVF:
             hi = min(L, lo + 4096)
             d2 = cn[None, :] - 2.0 * (self.cent[lo:hi] @ self.cent.T)
             lnbr[lo:hi] = torch.topk(d2, probe, dim=1, largest=False).indices
-        qorder = torch.argsort(qlist)
+        qorder = torch.sort(qlist, stable=True).indices
         qcounts = torch.bincount(qlist, minlength=L)
         qoff = torch.zeros(L + 1, dtype=torch.int64, device=dev)
         qoff[1:] = torch.cumsum(qcounts, 0)
@@ -277,7 +323,7 @@ def exact_knn_rescored(base: torch.Tensor, queries: torch.Tensor, k: int, pad: i
         order = torch.argsort(c, 1)
         c2 = torch.gather(c, 1, order)
         d2s = torch.gather(d2, 1, order)
-        o2 = torch.argsort(d2s, 1, stable=True)               # stable: ties keep id order
+        o2 = torch.sort(d2s, dim=1, stable=True).indices      # stable: ties keep id order
         out[lo:hi] = torch.gather(c2, 1, o2)[:, :k]
         del key
     return out

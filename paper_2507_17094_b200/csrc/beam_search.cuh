@@ -664,7 +664,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         __syncwarp();
 
         int32_t g_it = 0;
-        int64_t g_dc = 0, g_tv = 0;
+        int64_t g_dc = 0, g_tv = 0, g_ne = 0;
         int64_t n_logged = 0;
         bool has_entry = A.entries != nullptr;
         int32_t entry = has_entry ? A.entries[task] : -1;
@@ -679,6 +679,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
             g_it = (int32_t)S.c_it;
             g_dc = S.c_dc;
             g_tv = S.c_tv;
+            g_ne = S.c_ne;
             n_logged = 0;
         }
         // seeds (pipeline.py:227-231, search.py:294)
@@ -728,6 +729,8 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
                 A.st64[1 * A.st_stride + task] += S.c_tv + g_tv;
                 A.st64[2 * A.st_stride + task] += S.c_ins;
                 A.st64[3 * A.st_stride + task] += S.c_dgs;
+                A.st64[4 * A.st_stride + task] += S.c_ne;
+                A.st64[5 * A.st_stride + task] += g_ne;
             }
             if (A.rec) {
                 TaskRecord& R = A.rec[task];

@@ -131,11 +131,13 @@ struct pw_shard {
 namespace {
 
 template <typename T>
-int upload(T** dst, const void* src, size_t count, int64_t* bytes) {
-    if (count == 0) count = 1;
-    PW_CUDA(cudaMalloc((void**)dst, count * sizeof(T)));
-    if (src) PW_CUDA(cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
-    *bytes += (int64_t)(count * sizeof(T));
+int upload(T** dst, const void* src, size_t count, int64_t* bytes, bool on_device = false) {
+    size_t c = count == 0 ? 1 : count;
+    PW_CUDA(cudaMalloc((void**)dst, c * sizeof(T)));
+    if (src && count)
+        PW_CUDA(cudaMemcpy(*dst, src, count * sizeof(T),
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+    *bytes += (int64_t)(c * sizeof(T));
     return 0;
 }
 
@@ -430,19 +432,20 @@ int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
         pw_shard_destroy(sh);
         return code;
     };
-    if ((rc = upload(&sh->vec, D->vectors, (size_t)D->n * D->d, &sh->bytes))) return fail(rc);
-    if ((rc = upload(&sh->adj, D->adj, (size_t)D->n * D->j, &sh->bytes))) return fail(rc);
-    if ((rc = upload(&sh->gid, D->global_ids, (size_t)D->n, &sh->bytes))) return fail(rc);
+    const bool od = D->on_device != 0;
+    if ((rc = upload(&sh->vec, D->vectors, (size_t)D->n * D->d, &sh->bytes, od))) return fail(rc);
+    if ((rc = upload(&sh->adj, D->adj, (size_t)D->n * D->j, &sh->bytes, od))) return fail(rc);
+    if ((rc = upload(&sh->gid, D->global_ids, (size_t)D->n, &sh->bytes, od))) return fail(rc);
     if (D->direction &&
-        (rc = upload(&sh->dir, D->direction, (size_t)D->n * D->j * sh->W, &sh->bytes)))
+        (rc = upload(&sh->dir, D->direction, (size_t)D->n * D->j * sh->W, &sh->bytes, od)))
         return fail(rc);
-    if (D->inter_map && (rc = upload(&sh->inter, D->inter_map, (size_t)D->n, &sh->bytes)))
+    if (D->inter_map && (rc = upload(&sh->inter, D->inter_map, (size_t)D->n, &sh->bytes, od)))
         return fail(rc);
     if (D->ghost_n > 0) {
         sh->gn = D->ghost_n;
         sh->gj = D->ghost_j;
-        if ((rc = upload(&sh->gids, D->ghost_ids, (size_t)D->ghost_n, &sh->bytes))) return fail(rc);
-        if ((rc = upload(&sh->gadj, D->ghost_adj, (size_t)D->ghost_n * D->ghost_j, &sh->bytes)))
+        if ((rc = upload(&sh->gids, D->ghost_ids, (size_t)D->ghost_n, &sh->bytes, od))) return fail(rc);
+        if ((rc = upload(&sh->gadj, D->ghost_adj, (size_t)D->ghost_n * D->ghost_j, &sh->bytes, od)))
             return fail(rc);
         if ((rc = upload(&sh->gvec, nullptr, (size_t)D->ghost_n * D->d, &sh->bytes))) return fail(rc);
         gather_rows_kernel<<<256, 256>>>(sh->vec, sh->gids, sh->gn, sh->d, sh->gvec);
@@ -501,12 +504,15 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
 }
 
 int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q, int32_t n_cand,
-                   int32_t k, int32_t* final_ids, float* final_dists, void* stream) {
+                   int32_t k, int32_t* final_ids, float* final_dists, int32_t* err_dev,
+                   void* stream) {
     if (q <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    int32_t* err = nullptr;
-    PW_CUDA(cudaMallocAsync(&err, sizeof(int32_t), st));
-    PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    int32_t* err = err_dev;
+    if (!err) {
+        PW_CUDA(cudaMallocAsync(&err, sizeof(int32_t), st));
+        PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    }
     const int n = n_cand;
     const int warps = 4;
     size_t smem = (size_t)warps * n * sizeof(uint64_t);
@@ -517,6 +523,7 @@ int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q
                                                           final_dists, err);
     g_launches++;
     PW_CUDA(cudaGetLastError());
+    if (err_dev) return 0;
     int32_t herr = 0;
     PW_CUDA(cudaMemcpyAsync(&herr, err, sizeof herr, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaFreeAsync(err, st));
@@ -537,12 +544,12 @@ int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
     int rc = pw_fill_inf(shard_dists, q * N * k, st);                              // +inf padding
     if (rc) return rc;
     PW_CUDA(cudaMemsetAsync(stats_i32, 0, sizeof(int32_t) * 4 * q * N, st));
-    PW_CUDA(cudaMemsetAsync(stats_i64, 0, sizeof(int64_t) * 4 * q * N, st));
+    PW_CUDA(cudaMemsetAsync(stats_i64, 0, sizeof(int64_t) * 6 * q * N, st));
     if (mode == PW_MODE_BASELINE) {
         for (int s = 0; s < N; s++) {  // pipeline.py:288-297
             rc = pw_search_stage(shards[s], params, tuning, queries, 0, q, s, nullptr, nullptr,
                                  shard_ids, shard_dists, N, s, stats_i32 + (int64_t)s * 4 * q,
-                                 stats_i64 + (int64_t)s * 4 * q, q, st);
+                                 stats_i64 + (int64_t)s * 6 * q, q, st);
             if (rc) return rc;
         }
     } else {
@@ -561,7 +568,7 @@ int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
                                      stage, stage > 0 ? ein : nullptr,
                                      stage < N - 1 ? eout : nullptr, shard_ids, shard_dists, N, shard,
                                      stats_i32 + (int64_t)stage * 4 * q,
-                                     stats_i64 + (int64_t)stage * 4 * q, q, st);
+                                     stats_i64 + (int64_t)stage * 6 * q, q, st);
                 if (rc) return rc;
             }
             std::swap(ein, eout);
@@ -569,6 +576,16 @@ int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
     }
     return 0;
 }
+
+// Grow-only per-device workspace of pw_run (no allocation inside a steady
+// stream of calls, so end-to-end timings measure copies + kernels only).
+struct RunWs {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    char* buf = nullptr;
+    size_t cap = 0;
+};
+RunWs g_ws[64];
 
 int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw_tuning* tuning,
            const float* queries, int64_t q, int32_t mode, int32_t* shard_ids, float* shard_dists,
@@ -579,68 +596,61 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     if (rc) return rc;
     const int64_t k = params->k;
     const int32_t d = shards[0]->d;
-    cudaStream_t st;
-    PW_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    struct Bufs {
-        float* q = nullptr;
-        int32_t* sid = nullptr;
-        float* sd = nullptr;
-        int32_t* fid = nullptr;
-        float* fd = nullptr;
-        int32_t* s32 = nullptr;
-        int64_t* s64 = nullptr;
-        int32_t* ea = nullptr;
-        int32_t* eb = nullptr;
-    } B;
-    auto cleanup = [&]() {
-        void* ps[] = {B.q, B.sid, B.sd, B.fid, B.fd, B.s32, B.s64, B.ea, B.eb};
-        for (void* p : ps)
-            if (p) cudaFree(p);
-        cudaStreamDestroy(st);
-    };
-#define PW_TRY(call)                                                                         \
-    do {                                                                                     \
-        cudaError_t e_ = (call);                                                             \
-        if (e_ != cudaSuccess) {                                                             \
-            cleanup();                                                                       \
-            return set_err(e_ == cudaErrorMemoryAllocation ? PW_ENOMEM : PW_ECUDA,           \
-                           std::string(#call) + ": " + cudaGetErrorString(e_));             \
-        }                                                                                    \
-    } while (0)
-    const int64_t qq = std::max<int64_t>(q, 1);
-    PW_TRY(cudaMalloc(&B.q, sizeof(float) * qq * d));
-    PW_TRY(cudaMalloc(&B.sid, sizeof(int32_t) * qq * N * k));
-    PW_TRY(cudaMalloc(&B.sd, sizeof(float) * qq * N * k));
-    PW_TRY(cudaMalloc(&B.fid, sizeof(int32_t) * qq * k));
-    PW_TRY(cudaMalloc(&B.fd, sizeof(float) * qq * k));
-    PW_TRY(cudaMalloc(&B.s32, sizeof(int32_t) * qq * N * 4));
-    PW_TRY(cudaMalloc(&B.s64, sizeof(int64_t) * qq * N * 4));
-    PW_TRY(cudaMalloc(&B.ea, sizeof(int32_t) * qq));
-    PW_TRY(cudaMalloc(&B.eb, sizeof(int32_t) * qq));
-    PW_TRY(cudaMemcpyAsync(B.q, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
-    rc = pw_run_device(shards, N, params, tuning, B.q, q, mode, B.sid, B.sd, B.fid, B.fd, B.s32,
-                       B.s64, B.ea, B.eb, st);
-    if (rc == 0) rc = pw_reduce_topk(B.sid, B.sd, q, (int32_t)(N * k), (int32_t)k, B.fid, B.fd, st);
-    if (rc) {
-        std::string keep = g_err;
-        cleanup();
-        g_err = keep;
-        return rc;
-    }
-    PW_TRY(cudaMemcpyAsync(shard_ids, B.sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
-    PW_TRY(cudaMemcpyAsync(shard_dists, B.sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
-    PW_TRY(cudaMemcpyAsync(final_ids, B.fid, sizeof(int32_t) * q * k, cudaMemcpyDeviceToHost, st));
-    PW_TRY(cudaMemcpyAsync(final_dists, B.fd, sizeof(float) * q * k, cudaMemcpyDeviceToHost, st));
-    PW_TRY(cudaMemcpyAsync(stats_i32, B.s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
-    PW_TRY(cudaMemcpyAsync(stats_i64, B.s64, sizeof(int64_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
-    PW_TRY(cudaStreamSynchronize(st));
     for (int s = 0; s < N; s++)
-        if ((rc = check_err(shards[s]))) {
-            std::string keep = g_err;
-            cleanup();
-            g_err = keep;
-            return rc;
-        }
+        if (shards[s]->d != d || shards[s]->device != shards[0]->device)
+            return set_err(PW_EINVAL, "all shards of one pw_run must share d and device");
+    const int dev = shards[0]->device;
+    PW_CUDA(cudaSetDevice(dev));
+    RunWs& W = g_ws[dev];
+    std::lock_guard<std::mutex> lk(W.mu);
+    if (!W.st) PW_CUDA(cudaStreamCreateWithFlags(&W.st, cudaStreamNonBlocking));
+    cudaStream_t st = W.st;
+    const int64_t qq = std::max<int64_t>(q, 1);
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += (bytes + 255) / 256 * 256;
+        return o;
+    };
+    size_t o_q = take(sizeof(float) * qq * d), o_sid = take(sizeof(int32_t) * qq * N * k),
+           o_sd = take(sizeof(float) * qq * N * k), o_fid = take(sizeof(int32_t) * qq * k),
+           o_fd = take(sizeof(float) * qq * k), o_s32 = take(sizeof(int32_t) * qq * N * 4),
+           o_s64 = take(sizeof(int64_t) * qq * N * 6), o_ea = take(sizeof(int32_t) * qq),
+           o_eb = take(sizeof(int32_t) * qq), o_err = take(sizeof(int32_t));
+    if (W.cap < off) {
+        if (W.buf) cudaFree(W.buf);
+        W.buf = nullptr;
+        W.cap = 0;
+        PW_CUDA(cudaMalloc(&W.buf, off));
+        W.cap = off;
+    }
+    char* b = W.buf;
+    float* dq = (float*)(b + o_q);
+    int32_t* sid = (int32_t*)(b + o_sid);
+    float* sd = (float*)(b + o_sd);
+    int32_t* fid = (int32_t*)(b + o_fid);
+    float* fd = (float*)(b + o_fd);
+    int32_t* s32 = (int32_t*)(b + o_s32);
+    int64_t* s64 = (int64_t*)(b + o_s64);
+    int32_t* err = (int32_t*)(b + o_err);
+    PW_CUDA(cudaMemcpyAsync(dq, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
+    PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    rc = pw_run_device(shards, N, params, tuning, dq, q, mode, sid, sd, fid, fd, s32, s64,
+                       (int32_t*)(b + o_ea), (int32_t*)(b + o_eb), st);
+    if (rc) return rc;
+    if ((rc = pw_reduce_topk(sid, sd, q, (int32_t)(N * k), (int32_t)k, fid, fd, err, st))) return rc;
+    int32_t herr = 0;
+    PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(shard_dists, sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(final_ids, fid, sizeof(int32_t) * q * k, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(final_dists, fd, sizeof(float) * q * k, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(stats_i32, s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(stats_i64, s64, sizeof(int64_t) * q * N * 6, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(&herr, err, sizeof herr, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaStreamSynchronize(st));
+    for (int s = 0; s < N; s++)
+        if ((rc = check_err(shards[s]))) return rc;
+    if (herr) return set_err(PW_EINVAL, "cannot reduce empty candidate lists");
     // comm accounting (pipeline.py:340-341): 4 B per forwarded query
     std::memset(comm, 0, sizeof(int64_t) * N * N);
     if (mode == PW_MODE_PIPELINED) {
@@ -649,8 +659,6 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
         for (int stage = 0; stage < N - 1; stage++)
             for (int c = 0; c < N; c++) comm[(int64_t)stage * N + (c + stage) % N] = 4 * (lo[c + 1] - lo[c]);
     }
-    cleanup();
-#undef PW_TRY
     return 0;
 }
 

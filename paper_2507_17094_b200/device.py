@@ -1,0 +1,181 @@
+"""Device-resident search driver (shards built from torch tensors, outputs kept
+in HBM).  Same stage schedule as pipeline.run_* (pipeline.py:270-350), issued
+as asynchronous pw_search_stage launches on one CUDA stream; used by bench.py
+for the kernel-only timing and by ring.py for one-shard-per-GPU runs.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import weakref
+
+import numpy as np
+import torch
+
+from . import _abi
+
+STAT_I32 = ("iterations", "ghost_iterations", "retained", "converged")
+STAT_I64 = ("distance_computations", "total_visits", "inserted", "dgs_skipped",
+            "nodes_expanded", "ghost_nodes_expanded")
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+class TensorShard:
+    """A pw_shard created from device tensors (copied device-to-device)."""
+
+    def __init__(self, vectors: torch.Tensor, adj: torch.Tensor, global_ids: torch.Tensor,
+                 direction: torch.Tensor | None = None, inter_map: torch.Tensor | None = None,
+                 ghost_ids: torch.Tensor | None = None, ghost_adj: torch.Tensor | None = None):
+        lib = _abi.load()
+        torch.cuda.set_device(vectors.device)
+        self.device = vectors.device
+        vec = vectors.contiguous().float()
+        adj = adj.contiguous().to(torch.int32)
+        gid = global_ids.contiguous().to(torch.int32)
+        dr = None if direction is None else direction.contiguous().to(torch.int32)
+        it = None if inter_map is None else inter_map.contiguous().to(torch.int32)
+        gi = None if ghost_ids is None else ghost_ids.contiguous().to(torch.int32)
+        ga = None if ghost_adj is None else ghost_adj.contiguous().to(torch.int32)
+        torch.cuda.synchronize(self.device)
+        desc = _abi.ShardDesc(vec.shape[0], vec.shape[1], adj.shape[1], 0, _ptr(vec), _ptr(adj),
+                              _ptr(gid), _ptr(dr), _ptr(it), 0 if gi is None else gi.shape[0],
+                              0 if ga is None else ga.shape[1], _ptr(gi), _ptr(ga), 1)
+        h = C.c_void_p()
+        _abi.check(lib.pw_shard_create(C.byref(desc), C.byref(h)))
+        self.handle = h
+        self.n, self.d = vec.shape
+        self.j = adj.shape[1]
+        self.W = (self.d + 31) // 32
+        self.ghost_n = 0 if gi is None else gi.shape[0]
+        self.ghost_j = 0 if ga is None else ga.shape[1]
+        self.has_inter = it is not None
+        self.nbytes = int(lib.pw_shard_bytes(h))
+        self._finalizer = weakref.finalize(self, lib.pw_shard_destroy, h)
+
+
+class DeviceRun:
+    """Preallocated device outputs for Q queries over n_cols shard columns."""
+
+    def __init__(self, q: int, n_cols: int, k: int, device):
+        self.q, self.n_cols, self.k = q, n_cols, k
+        dev = torch.device(device)
+        self.shard_ids = torch.empty((q, n_cols, k), dtype=torch.int32, device=dev)
+        self.shard_dists = torch.empty((q, n_cols, k), dtype=torch.float32, device=dev)
+        self.final_ids = torch.empty((q, k), dtype=torch.int32, device=dev)
+        self.final_dists = torch.empty((q, k), dtype=torch.float32, device=dev)
+        self.s32 = torch.empty((n_cols, 4, q), dtype=torch.int32, device=dev)
+        self.s64 = torch.empty((n_cols, 6, q), dtype=torch.int64, device=dev)
+        self.entries = [torch.zeros(q, dtype=torch.int32, device=dev) for _ in range(2)]
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def reset(self):
+        self.shard_ids.fill_(-1)
+        self.shard_dists.fill_(float("inf"))
+        self.s32.zero_()
+        self.s64.zero_()
+
+    def stats(self) -> list[dict]:
+        s32 = self.s32.cpu().numpy()
+        s64 = self.s64.cpu().numpy()
+        out = []
+        for s in range(self.n_cols):
+            st = {name: s32[s, i] for i, name in enumerate(STAT_I32)}
+            st.update({name: s64[s, i] for i, name in enumerate(STAT_I64)})
+            out.append(st)
+        return out
+
+
+def search_stage(shard: TensorShard, params, queries: torch.Tensor, q0: int, n: int, stage: int,
+                 run: DeviceRun, col: int, stat_row: int, entries_in=None, forward_out=None,
+                 tuning=None, stream=None) -> None:
+    """One pw_search_stage launch (asynchronous on `stream`)."""
+    lib = _abi.load()
+    p = _abi.params_struct(params)
+    t = _abi.tuning_struct(tuning)
+    st = (stream or torch.cuda.current_stream(queries.device)).cuda_stream
+    s32 = run.s32[stat_row]
+    s64 = run.s64[stat_row]
+    _abi.check(lib.pw_search_stage(shard.handle, C.byref(p), C.byref(t), queries.data_ptr(), q0, n,
+                                   stage, _ptr(entries_in), _ptr(forward_out),
+                                   run.shard_ids.data_ptr(), run.shard_dists.data_ptr(), run.n_cols,
+                                   col, s32.data_ptr(), s64.data_ptr(), run.q, st))
+
+
+def reduce(run: DeviceRun, stream=None) -> None:
+    lib = _abi.load()
+    st = (stream or torch.cuda.current_stream(run.final_ids.device)).cuda_stream
+    _abi.check(lib.pw_reduce_topk(run.shard_ids.data_ptr(), run.shard_dists.data_ptr(), run.q,
+                                  run.n_cols * run.k, run.k, run.final_ids.data_ptr(),
+                                  run.final_dists.data_ptr(), run.err.data_ptr(), st))
+
+
+def chunk_bounds(q: int, n: int) -> list[int]:
+    """np.array_split(arange(q), n) boundaries (pipeline.py:327)."""
+    lo = [0]
+    for c in range(n):
+        lo.append(lo[-1] + q // n + (1 if c < q % n else 0))
+    return lo
+
+
+def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: str, run: DeviceRun,
+              tuning=None, stream=None, timer: list | None = None) -> None:
+    """All shards on this device: baseline (shard s = stage s, all queries) or
+    pipelined (chunk c stage s on shard (c+s)%N, entry forwarded in HBM).
+    If `timer` is a list, (start, end) CUDA events bracket every search launch."""
+    n = len(shards)
+    q = queries.shape[0]
+    stream = stream or torch.cuda.current_stream(queries.device)
+
+    def launch(*a, **kw):
+        if timer is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        search_stage(*a, tuning=tuning, stream=stream, **kw)
+        if timer is not None:
+            e1.record(stream)
+            timer.append((e0, e1))
+
+    with torch.cuda.stream(stream):
+        run.reset()
+    if mode == "baseline":
+        for s in range(n):
+            launch(shards[s], params, queries, 0, q, s, run, s, s)
+    else:
+        lo = chunk_bounds(q, n)
+        ein, eout = run.entries
+        for stage in range(n):
+            for c in range(n):
+                shard = (c + stage) % n
+                launch(shards[shard], params, queries, lo[c], lo[c + 1] - lo[c], stage, run, shard,
+                       stage, entries_in=ein if stage > 0 else None,
+                       forward_out=eout if stage < n - 1 else None)
+            ein, eout = eout, ein
+    reduce(run, stream)
+
+
+def algorithmic_bytes(stats: list[dict], params, d: int, j: int, j_g: int, esize: int = 4,
+                      seeded_stages: set | None = None) -> float:
+    """Gather bytes the search path must read (per query summed):
+    DC*d*s_e + (E + S)*j*4 + E_ghost*j_g*4 + P*(j*W*4 + d*s_e)
+    with P = pruned expansions = dgs_skipped / (j - n_keep) (each pruned parent
+    reads its direction row and its own vector, search.py:257-258) and S = 1
+    per neighbour-seeded search (adj[entry] read, pipeline.py:231)."""
+    W = (d + 31) // 32
+    n_keep = max(1, int((1.0 - params.discard_ratio) * j + 0.5))
+    total = 0.0
+    for s, st in enumerate(stats):
+        dc = float(st["distance_computations"].sum())
+        e = float(st["nodes_expanded"].sum())
+        eg = float(st["ghost_nodes_expanded"].sum())
+        pruned = float(st["dgs_skipped"].sum()) / (j - n_keep) if j > n_keep else 0.0
+        seeded = 0.0
+        if params.seed_mode == "neighbors":
+            seeded = float((st["ghost_iterations"] > 0).sum())
+            if seeded_stages and s in seeded_stages:
+                seeded = float(len(st["iterations"]))
+        total += dc * d * esize + (e + seeded) * j * 4 + eg * j_g * 4 + pruned * (j * W * 4 + d * esize)
+    return total

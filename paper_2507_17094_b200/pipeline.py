@@ -164,7 +164,7 @@ def reduce_topk(ids: np.ndarray, dists: np.ndarray, k: int):
     od = torch.empty(k, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev).cuda_stream
     _abi.check(lib.pw_reduce_topk(ti.data_ptr(), td.data_ptr(), 1, ids.size, k, oi.data_ptr(),
-                                  od.data_ptr(), stream))
+                                  od.data_ptr(), None, stream))
     oi, od = oi.cpu().numpy(), od.cpu().numpy()
     n = int((oi >= 0).sum())
     return oi[:n].astype(np.int32), od[:n].astype(np.float32)
@@ -198,7 +198,7 @@ def _run(mode: str, queries, index, dataset, params: SearchParams, contexts, tun
     final_ids = np.empty((q, k), np.int32)
     final_dists = np.empty((q, k), np.float32)
     s32 = np.empty((n, 4, q), np.int32)
-    s64 = np.empty((n, 4, q), np.int64)
+    s64 = np.empty((n, 6, q), np.int64)
     comm = np.empty((n, n), np.int64)
     _abi.check(lib.pw_run(handles, n, C.byref(p), C.byref(t), qdata.ctypes.data, q,
                           _abi.MODE[mode], shard_ids.ctypes.data, shard_dists.ctypes.data,

@@ -1,0 +1,175 @@
+"""One shard per GPU: the ring of pipelining-based path extension
+(shardann/pipeline.py:308-385) and the naive sharded baseline (:270-305)
+across processes, one process per GPU over torch.distributed (NCCL on GPUs,
+gloo in the CPU tests).
+
+Pipelined schedule (pipeline.py:327-342): queries are split into N chunks;
+at stage s rank g searches chunk (g - s) mod N on its shard g, then sends the
+chunk's forward entries (inter_map_g[top1], one int32 per query -- the only
+payload that crosses a link, pipeline.py:339-341) to rank g+1, which seeds
+stage s+1 of the same chunk with them.  Every rank is busy at every stage.
+After the last stage each rank holds the shard-g column of every query's
+candidate list; an all-gather assembles the (Q, N, k) lists and K2 reduces
+them (pipeline.py:249-267).  Baseline: every rank searches every query on
+its shard (stage index = shard index), then the same all-gather + reduce.
+
+The per-stage search is pluggable (``stage_fn``) so the CPU tests drive this
+exact schedule with the oracle over gloo.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def chunk_bounds(q: int, n: int) -> list[int]:
+    """np.array_split(arange(q), n) boundaries (pipeline.py:327)."""
+    lo = [0]
+    for c in range(n):
+        lo.append(lo[-1] + q // n + (1 if c < q % n else 0))
+    return lo
+
+
+def ring_schedule(rank: int, world: int, stage: int) -> int:
+    """Chunk processed by `rank` at `stage`: shard (c + s) % N == rank."""
+    return (rank - stage) % world
+
+
+def comm_stage_bytes(q: int, world: int) -> np.ndarray:
+    """pipeline.py:340-341 accounting: (N_stages, N) bytes sent by each shard."""
+    lo = chunk_bounds(q, world)
+    out = np.zeros((world, world), np.int64)
+    for stage in range(world - 1):
+        for c in range(world):
+            out[stage, (c + stage) % world] = 4 * (lo[c + 1] - lo[c])
+    return out
+
+
+def run_ring_pipelined(stage_fn, q: int, rank: int, world: int, send_recv, on_stage_done=None):
+    """Drive the pipelined ring for this rank.
+
+    stage_fn(stage, q0, n, entries_or_None) -> forward entries (n,) int32 or None
+    send_recv(send_array, recv_count) -> received array (exchange with g+1 / g-1)
+    """
+    lo = chunk_bounds(q, world)
+    entries = None
+    for stage in range(world):
+        c = ring_schedule(rank, world, stage)
+        fwd = stage_fn(stage, lo[c], lo[c + 1] - lo[c], entries)
+        if stage < world - 1:
+            c_next = ring_schedule(rank, world, stage + 1)
+            entries = send_recv(fwd, lo[c_next + 1] - lo[c_next])
+        if on_stage_done is not None:
+            on_stage_done(stage)
+
+
+class RingSearch:
+    """Device engine of one rank (one shard on this GPU)."""
+
+    def __init__(self, shard, q: int, k: int, rank: int, world: int, device):
+        import torch
+
+        from . import device as dv
+
+        self.shard, self.q, self.k, self.rank, self.world = shard, q, k, rank, world
+        self.dev = torch.device(device)
+        self.run_buf = dv.DeviceRun(q, world, k, self.dev)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self._lib = None
+
+    # ---------------------------------------------------------------- device path
+    def run(self, queries, params, mode: str, timer: list | None = None) -> np.ndarray | None:
+        """Search all queries; returns final ids (Q, k) numpy on rank 0."""
+        import torch
+        import torch.distributed as dist
+
+        from . import device as dv
+
+        R = self.run_buf
+        if self.world == 1:
+            dv.run_local([self.shard], params, queries, mode, R, stream=self.stream, timer=timer)
+            return R.final_ids.cpu().numpy()
+
+        R.reset()
+        g, N = self.rank, self.world
+
+        def launch(stage, q0, n, entries_in, forward_out):
+            if timer is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(self.stream)
+            dv.search_stage(self.shard, params, queries, q0, n, stage, R, g, stage,
+                            entries_in=entries_in, forward_out=forward_out, stream=self.stream)
+            if timer is not None:
+                e1.record(self.stream)
+                timer.append((e0, e1))
+
+        if mode == "baseline":
+            launch(g, 0, self.q, None, None)
+        else:
+            ein, eout = R.entries
+            lo = chunk_bounds(self.q, N)
+            for stage in range(N):
+                c = ring_schedule(g, N, stage)
+                launch(stage, lo[c], lo[c + 1] - lo[c], ein if stage > 0 else None,
+                       eout if stage < N - 1 else None)
+                if stage < N - 1:
+                    cn = ring_schedule(g, N, stage + 1)
+                    send = eout[lo[c]:lo[c + 1]]
+                    recv = ein[lo[cn]:lo[cn + 1]]
+                    ops = [dist.P2POp(dist.isend, send, (g + 1) % N),
+                           dist.P2POp(dist.irecv, recv, (g - 1) % N)]
+                    for w in dist.batch_isend_irecv(ops):
+                        w.wait()
+        # all-gather this rank's column of the candidate lists, then reduce (K2)
+        col_ids = R.shard_ids[:, g, :].contiguous()
+        col_d = R.shard_dists[:, g, :].contiguous()
+        all_ids = torch.empty((N,) + tuple(col_ids.shape), dtype=col_ids.dtype, device=self.dev)
+        all_d = torch.empty((N,) + tuple(col_d.shape), dtype=col_d.dtype, device=self.dev)
+        dist.all_gather_into_tensor(all_ids, col_ids)
+        dist.all_gather_into_tensor(all_d, col_d)
+        R.shard_ids.copy_(all_ids.permute(1, 0, 2))
+        R.shard_dists.copy_(all_d.permute(1, 0, 2))
+        dv.reduce(R, self.stream)
+        return R.final_ids.cpu().numpy() if self.rank == 0 else None
+
+    def last_stats(self) -> list[dict]:
+        return self.run_buf.stats()
+
+    # ---------------------------------------------------------------- host (e2e) path
+    def run_host(self, queries_host: np.ndarray, params) -> dict:
+        """End-to-end through the C ABI with host buffers (N=1: pw_run)."""
+        import ctypes as C
+
+        from . import _abi
+
+        if self.world == 1:
+            lib = _abi.load()
+            q = queries_host.shape[0]
+            k = int(params.k)
+            out = dict(shard_ids=np.empty((q, 1, k), np.int32),
+                       shard_dists=np.empty((q, 1, k), np.float32),
+                       final_ids=np.empty((q, k), np.int32), final_dists=np.empty((q, k), np.float32),
+                       s32=np.empty((1, 4, q), np.int32), s64=np.empty((1, 6, q), np.int64),
+                       comm=np.empty((1, 1), np.int64))
+            handles = (C.c_void_p * 1)(self.shard.handle.value)
+            p = _abi.params_struct(params)
+            t = _abi.tuning_struct(None)
+            _abi.check(lib.pw_run(handles, 1, C.byref(p), C.byref(t), queries_host.ctypes.data, q,
+                                  _abi.MODE["pipelined"], out["shard_ids"].ctypes.data,
+                                  out["shard_dists"].ctypes.data, out["final_ids"].ctypes.data,
+                                  out["final_dists"].ctypes.data, out["s32"].ctypes.data,
+                                  out["s64"].ctypes.data, out["comm"].ctypes.data))
+            out["bytes_out"] = sum(v.nbytes for key, v in out.items() if key != "comm")
+            return out
+        import torch
+
+        qd = torch.from_numpy(queries_host).to(self.dev, non_blocking=False)
+        ids = self.run(qd, params, "pipelined")
+        out = {"final_ids": ids}
+        if self.rank == 0:
+            out["final_dists"] = self.run_buf.final_dists.cpu().numpy()
+            out["bytes_out"] = out["final_ids"].nbytes + out["final_dists"].nbytes
+        else:
+            out["bytes_out"] = 0
+        return out

@@ -158,7 +158,7 @@ class DeviceShard:
             gid.ctypes.data, None if direction is None else direction.ctypes.data,
             None if inter is None else inter.ctypes.data,
             0 if gids is None else gids.shape[0], 0 if gadj is None else gadj.shape[1],
-            None if gids is None else gids.ctypes.data, None if gadj is None else gadj.ctypes.data)
+            None if gids is None else gids.ctypes.data, None if gadj is None else gadj.ctypes.data, 0)
         h = C.c_void_p()
         _abi.check(lib.pw_shard_create(C.byref(desc), C.byref(h)))
         self.handle = h
