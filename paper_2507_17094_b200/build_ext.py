@@ -1,6 +1,10 @@
-"""Compile libpwb200.so in-tree for sm_100a (nvcc, no torch extension machinery).
+"""Compile libpwb200.so in-tree for sm_100a (nvcc; no torch extension machinery).
 
-    python -m paper_2507_17094_b200.build_ext
+K1 is specialised per vector dimension (compile-time pairwise order + TMA row
+gathers); each specialisation is its own translation unit (csrc/k_inst.cu with
+-DPW_DIM=d), compiled in parallel and linked with the host ABI (pw_abi.cu).
+
+    python -m paper_2507_17094_b200.build_ext [--force]
 """
 
 from __future__ import annotations
@@ -9,20 +13,20 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-SOURCES = [PKG / "csrc" / "pw_abi.cu"]
-DEPS = SOURCES + sorted((PKG / "csrc").glob("*.cuh")) + [ROOT / "include" / "pw_b200.h"]
+CSRC = PKG / "csrc"
+BUILD = PKG / "_build"
 OUT = PKG / "libpwb200.so"
+# must match PW_DIMS in csrc/pw_abi.cu (0 = generic d)
+DIMS = (0, 16, 32, 64, 96, 100, 128, 200, 256, 384, 512, 768, 960, 1024)
+DEPS = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "pw_b200.h"]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
-    "-Xptxas", "-v",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc() -> str:
@@ -39,20 +43,36 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
-        return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(OUT) + ".tmp", *map(str, SOURCES)]
+def _run(cmd):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed: " + " ".join(cmd))
+        raise RuntimeError("nvcc failed: " + " ".join(map(str, cmd)))
+    return r.stderr
+
+
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
+    if not force and up_to_date():
+        return OUT
+    BUILD.mkdir(exist_ok=True)
+    nv = nvcc()
+    jobs_list = [([nv, *CFLAGS, "-c", str(CSRC / "pw_abi.cu"), "-o", str(BUILD / "pw_abi.o")],
+                  BUILD / "pw_abi.o")]
+    for d in DIMS:
+        obj = BUILD / f"k_{d}.o"
+        jobs_list.append(([nv, *CFLAGS, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",
+                           str(obj)], obj))
+    workers = jobs or max(1, min(len(jobs_list), os.cpu_count() or 1))
+    with ThreadPoolExecutor(workers) as pool:
+        logs = list(pool.map(lambda j: _run(j[0]), jobs_list))
+    objs = [str(o) for _, o in jobs_list]
+    _run([nv, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(OUT) + ".tmp", *objs])
     os.replace(str(OUT) + ".tmp", OUT)
-    (PKG / "build_ptxas.log").write_text(r.stderr)
+    (PKG / "build_ptxas.log").write_text("\n".join(logs))
     if verbose:
-        print(r.stderr)
+        print("\n".join(logs))
     return OUT
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -94,7 +94,9 @@ struct KArgs {
     // per-warp shared-memory layout (bytes)
     int32_t L_max, CB, BH, H, R, PG;
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
-        o_misc, warp_bytes;
+        o_misc, o_mbar, warp_bytes;
+    int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
+    int32_t bulk_adj;       // adjacency / direction rows may use cp.async.bulk
     int32_t vis_limit;      // smem visited entries before spilling to global
     uint32_t* gvis;         // per-warp global visited tables
     int32_t gmask;
@@ -129,6 +131,69 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---- TMA bulk copies (cp.async.bulk, SASS UBLKCP) completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ---- warp-wide bitonic sorts (ascending across lanes)
+__device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            uint64_t o = __shfl_xor_sync(0xffffffffu, x, j);
+            bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+            x = keep_min ? (o < x ? o : x) : (o > x ? o : x);
+        }
+    return x;
+}
+__device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            uint32_t o = __shfl_xor_sync(0xffffffffu, x, j);
+            bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
+            x = keep_min ? min(o, x) : max(o, x);
+        }
+    return x;
 }
 
 // Warp-cooperative async copy of `bytes` (multiple of 4) into shared memory.
@@ -189,6 +254,53 @@ __device__ __forceinline__ float l2_row(const L2Plan& P, const float* x, const f
     return stack[0];
 }
 
+// Compile-time numpy pairwise order for row length N at offset OFF, lane
+// layout (row v = lane>>1, half h = lane&1): half h owns accumulators
+// 4h..4h+3 and reads them as one float4 per 8-element step.
+template <int OFF, int N>
+__device__ __forceinline__ float pw_leaf(const float* x, const float* q, unsigned h) {
+    if constexpr (N < 8) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
+        return s;
+    } else {
+        constexpr int NF = N - (N % 8);
+        const float4* x4 = reinterpret_cast<const float4*>(x + OFF);
+        const float4* q4 = reinterpret_cast<const float4*>(q + OFF);
+        float4 xv = x4[h], qv = q4[h];
+        float r0 = sqd(xv.x, qv.x), r1 = sqd(xv.y, qv.y), r2 = sqd(xv.z, qv.z), r3 = sqd(xv.w, qv.w);
+#pragma unroll
+        for (int p = 1; p < NF / 8; p++) {
+            xv = x4[2 * p + h];
+            qv = q4[2 * p + h];
+            r0 = __fadd_rn(r0, sqd(xv.x, qv.x));
+            r1 = __fadd_rn(r1, sqd(xv.y, qv.y));
+            r2 = __fadd_rn(r2, sqd(xv.z, qv.z));
+            r3 = __fadd_rn(r3, sqd(xv.w, qv.w));
+        }
+        // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)): IEEE add is commutative, so
+        // both halves end with the bit-identical value
+        float a = __fadd_rn(__fadd_rn(r0, r1), __fadd_rn(r2, r3));
+        float s = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+#pragma unroll
+        for (int i = NF; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
+        return s;
+    }
+}
+
+template <int OFF, int N>
+__device__ __forceinline__ float pw_sum(const float* x, const float* q, unsigned h) {
+    if constexpr (N <= 128) {
+        return pw_leaf<OFF, N>(x, q, h);
+    } else {
+        constexpr int N2 = N / 2 - (N / 2) % 8;
+        float a = pw_sum<OFF, N2>(x, q, h);
+        float b = pw_sum<OFF + N2, N - N2>(x, q, h);
+        return __fadd_rn(a, b);
+    }
+}
+
 // --------------------------------------------------------------- per warp
 struct WarpState {
     float* q;
@@ -205,6 +317,8 @@ struct WarpState {
     int32_t* misc;
     uint32_t* gvis;
     uint32_t* gscr;
+    uint64_t* mbar;         // [0],[1] gather halves, [2] expansion fetch
+    uint32_t phase;         // parity bit per mbarrier
     int32_t cur;            // current queue buffer
     int32_t qlen;
     int32_t vcount;         // entries in the smem visited table
@@ -247,7 +361,7 @@ __device__ __forceinline__ void bh_clear(const KArgs& A, WarpState& S) {
 // Ordered first-occurrence dedup of src[0..n) keeping the first `limit`
 // unique ids, written to dst (search.py:219 dict.fromkeys / :230-232
 // _ordered_unique + [:cap]).  Returns the kept count; bh stays populated.
-__device__ int dedup_ordered(const KArgs& A, WarpState& S, const int32_t* src, int n, int limit,
+static __device__ int dedup_ordered(const KArgs& A, WarpState& S, const int32_t* src, int n, int limit,
                              int32_t* dst, int* n_unique) {
     const unsigned lane = lane_id();
     for (int t = lane; t < n; t += 32) {
@@ -304,7 +418,7 @@ __device__ __forceinline__ bool visit_insert(const KArgs& A, WarpState& S, uint3
 }
 
 // Keep only never-scored ids of newl[0..nb) (in order); returns n_new.
-__device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
+static __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
     const unsigned lane = lane_id();
     if (!S.ovf && S.vcount + nb > A.vis_limit) {
         S.ovf = true;
@@ -327,51 +441,96 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
 }
 
 // Gather rows newl[0..n) and compute exact squared L2 keys into ckey.
+// D > 0: rows land in shared memory by TMA bulk copies (one lane per row,
+// completion on a per-half mbarrier, two halves in flight), and 16 rows are
+// reduced per warp pass in the compile-time pairwise order.  D == 0: generic
+// d (cp.async + runtime pairwise plan).
+template <int D>
 __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n) {
     const unsigned lane = lane_id();
     const int RH = A.R >> 1;
-    const int row_bytes = A.d * 4;
     const int sp = A.spad;
     const int ngroups = (n + RH - 1) / RH;
-    auto issue = [&](int g) {
-        if (g < ngroups) {
+    if constexpr (D > 0) {
+        constexpr uint32_t row_bytes = D * 4;
+        auto issue = [&](int g) {
+            if (g >= ngroups) return;
+            const int r0 = g * RH;
+            const int rows = min(RH, n - r0);
+            float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
+            uint64_t* bar = S.mbar + (g & 1);
+            fence_proxy_async();
+            if (lane == 0) mbar_arrive_expect(bar, rows * row_bytes);
+            __syncwarp();
+            for (int r = lane; r < rows; r += 32) {
+                const int32_t id = S.newl[r0 + r];
+                bulk_g2s(dst0 + (size_t)r * sp, G.vec + (size_t)id * D, row_bytes, bar);
+            }
+        };
+        issue(0);
+        issue(1);
+        const unsigned v = lane >> 1, h = lane & 1u;
+        for (int g = 0; g < ngroups; g++) {
+            mbar_wait(S.mbar + (g & 1), (S.phase >> (g & 1)) & 1u);
+            S.phase ^= 1u << (g & 1);
+            const int r0 = g * RH;
+            const int rows = min(RH, n - r0);
+            const float* base = S.stage + (size_t)(g & 1) * RH * sp;
+            for (int pass = 0; pass < rows; pass += 16) {
+                const int rr = pass + (int)v;
+                const int rc = rr < rows ? rr : rows - 1;
+                const float dist = pw_sum<0, D>(base + (size_t)rc * sp, S.q, h);
+                if (h == 0 && rr < rows) {
+                    const uint32_t id = (uint32_t)S.newl[r0 + rr];
+                    S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
+                }
+            }
+            __syncwarp();
+            issue(g + 2);
+        }
+        __syncwarp();
+    } else {
+        const int row_bytes = A.d * 4;
+        auto issue = [&](int g) {
+            if (g < ngroups) {
+                int r0 = g * RH;
+                int rows = min(RH, n - r0);
+                float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
+                for (int r = 0; r < rows; r++) {
+                    int32_t id = S.newl[r0 + r];
+                    warp_copy_async(dst0 + (size_t)r * sp, G.vec + (size_t)id * A.d, row_bytes);
+                }
+            }
+            cp_commit();
+        };
+        issue(0);
+        issue(1);
+        const unsigned v = lane >> 3, a = lane & 7u;
+        for (int g = 0; g < ngroups; g++) {
+            cp_wait<1>();
+            __syncwarp();
             int r0 = g * RH;
             int rows = min(RH, n - r0);
-            float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
-            for (int r = 0; r < rows; r++) {
-                int32_t id = S.newl[r0 + r];
-                warp_copy_async(dst0 + (size_t)r * sp, G.vec + (size_t)id * A.d, row_bytes);
+            const float* base = S.stage + (size_t)(g & 1) * RH * sp;
+            for (int sub = 0; sub < rows; sub += 4) {
+                int rr = sub + (int)v;
+                int rc = rr < rows ? rr : rows - 1;
+                float dist = l2_row(A.plan, base + (size_t)rc * sp, S.q, a);
+                if (a == 0 && rr < rows) {
+                    uint32_t id = (uint32_t)S.newl[r0 + rr];
+                    S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
+                }
             }
+            __syncwarp();
+            issue(g + 2);
         }
-        cp_commit();
-    };
-    issue(0);
-    issue(1);
-    const unsigned v = lane >> 3, a = lane & 7u;
-    for (int g = 0; g < ngroups; g++) {
-        cp_wait<1>();
+        cp_wait<0>();
         __syncwarp();
-        int r0 = g * RH;
-        int rows = min(RH, n - r0);
-        const float* base = S.stage + (size_t)(g & 1) * RH * sp;
-        for (int sub = 0; sub < rows; sub += 4) {
-            int rr = sub + (int)v;
-            int rc = rr < rows ? rr : rows - 1;
-            float dist = l2_row(A.plan, base + (size_t)rc * sp, S.q, a);
-            if (a == 0 && rr < rows) {
-                uint32_t id = (uint32_t)S.newl[r0 + rr];
-                S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
-            }
-        }
-        __syncwarp();
-        issue(g + 2);
     }
-    cp_wait<0>();
-    __syncwarp();
 }
 
 // search.py:170-190 merge_and_sort on keys; returns `inserted`.
-__device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int n) {
+static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int n) {
     const unsigned lane = lane_id();
     const int L = C.L;
     const uint64_t* qk = S.qk[S.cur];
@@ -393,6 +552,47 @@ __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int
     }
     __syncwarp();
     if (s == 0) return 0;
+    if (s <= 32) {
+        // bitonic-sort the survivors across the warp, then merge-path positions
+        uint64_t mine = (int)lane < s ? S.ckey[lane] : ~0ull;
+        mine = warp_sort_u64(mine);
+        if ((int)lane < s) S.ckey[lane] = mine;
+        __syncwarp();
+        for (int t = lane; t < qlen; t += 32) {
+            const uint64_t key = qk[t];
+            int lo = 0, hi = s;  // survivors smaller than key
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (S.ckey[mid] < key) lo = mid + 1;
+                else hi = mid;
+            }
+            const int np = t + lo;
+            if (np < L) {
+                nk[np] = key;
+                ne[np] = qe[t];
+            }
+        }
+        bool kept = false;
+        if ((int)lane < s) {
+            int lo = 0, hi = qlen;
+            while (lo < hi) {
+                int mid = (lo + hi) >> 1;
+                if (qk[mid] < mine) lo = mid + 1;
+                else hi = mid;
+            }
+            const int p = (int)lane + lo;
+            if (p < L) {
+                nk[p] = mine;
+                ne[p] = 0;
+                kept = true;
+            }
+        }
+        const int ins = __popc(__ballot_sync(0xffffffffu, kept));
+        __syncwarp();
+        S.qlen = min(L, qlen + s);
+        S.cur ^= 1;
+        return ins;
+    }
     // queue entries: shift by number of smaller survivors
     for (int t = lane; t < qlen; t += 32) {
         uint64_t key = qk[t];
@@ -435,7 +635,7 @@ __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int
 }
 
 // search.py:192-204: first r unexpanded queue entries, marked expanded.
-__device__ int select_parents(WarpState& S, int r, int32_t* parents) {
+static __device__ int select_parents(WarpState& S, int r, int32_t* parents) {
     const unsigned lane = lane_id();
     uint64_t* qk = S.qk[S.cur];
     uint8_t* qe = S.qe[S.cur];
@@ -457,18 +657,55 @@ __device__ int select_parents(WarpState& S, int r, int32_t* parents) {
 
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
 // returns the candidate count p * n_sel.
-__device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
+// Fetch up to 3 row sets (adjacency, parent vectors, direction rows) for the
+// parents in ONE round trip: TMA bulk copies when aligned (one lane per row),
+// else cp.async.
+template <typename F>
+__device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_rows, uint32_t total,
+                                            F&& row) {
+    const unsigned lane = lane_id();
+    if (A.bulk_adj) {
+        fence_proxy_async();
+        if (lane == 0) mbar_arrive_expect(S.mbar + 2, total);
+        __syncwarp();
+        for (int r = lane; r < n_rows; r += 32) {
+            void* dst;
+            const void* src;
+            uint32_t bytes;
+            row(r, dst, src, bytes);
+            bulk_g2s(dst, src, bytes, S.mbar + 2);
+        }
+        mbar_wait(S.mbar + 2, (S.phase >> 2) & 1u);
+        S.phase ^= 4u;
+    } else {
+        for (int r = 0; r < n_rows; r++) {
+            void* dst;
+            const void* src;
+            uint32_t bytes;
+            row(r, dst, src, bytes);
+            warp_copy_async(dst, src, (int)bytes);
+        }
+        cp_commit();
+        cp_wait<0>();
+    }
+    __syncwarp();
+}
+
+// _expand (search.py:235-266) up to the ordered candidate list in S.cand;
+// returns the candidate count p * n_sel.
+static __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                       const int32_t* parents, int np, int it, Pcg64& rng) {
     const unsigned lane = lane_id();
     const int j = G.j;
     if (j == 0) return 0;
     const bool prune = C.prune_sel != 0 && it < C.cool_start;
+    const uint32_t adj_bytes = (uint32_t)j * 4u;
     if (!prune) {
-        for (int pi = 0; pi < np; pi++)
-            warp_copy_async(S.cand + pi * j, G.adj + (size_t)parents[pi] * j, j * 4);
-        cp_commit();
-        cp_wait<0>();
-        __syncwarp();
+        fetch_group(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
+            dst = S.cand + r * j;
+            src = G.adj + (size_t)parents[r] * j;
+            b = adj_bytes;
+        });
         return np * j;
     }
     const int nsel = C.n_keep < j ? C.n_keep : j;
@@ -478,19 +715,29 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
     uint32_t* qb = reinterpret_cast<uint32_t*>(S.misc + A.PG * j);  // PG * W
     if (C.prune_sel == 1) {
         const int W = A.W, d = A.d;
+        const uint32_t vec_bytes = (uint32_t)d * 4u, dir_bytes = (uint32_t)(j * W) * 4u;
         for (int pg = 0; pg < np; pg += A.PG) {
             const int gp = min(A.PG, np - pg);
             float* prow = S.stage;
             uint32_t* drow = reinterpret_cast<uint32_t*>(S.stage + (size_t)gp * A.spad);
-            for (int pi = 0; pi < gp; pi++) {
-                const int32_t par = parents[pg + pi];
-                warp_copy_async(craw + (pg + pi) * j, G.adj + (size_t)par * j, j * 4);
-                warp_copy_async(prow + (size_t)pi * A.spad, G.vec + (size_t)par * d, d * 4);
-                warp_copy_async(drow + (size_t)pi * j * W, G.dir + (size_t)par * j * W, j * W * 4);
-            }
-            cp_commit();
-            cp_wait<0>();
-            __syncwarp();
+            fetch_group(A, S, 3 * gp, gp * (adj_bytes + vec_bytes + dir_bytes),
+                        [&](int r, void*& dst, const void*& src, uint32_t& b) {
+                            const int pi = r % gp, kind = r / gp;
+                            const int32_t par = parents[pg + pi];
+                            if (kind == 0) {
+                                dst = craw + (pg + pi) * j;
+                                src = G.adj + (size_t)par * j;
+                                b = adj_bytes;
+                            } else if (kind == 1) {
+                                dst = prow + (size_t)pi * A.spad;
+                                src = G.vec + (size_t)par * d;
+                                b = vec_bytes;
+                            } else {
+                                dst = drow + (size_t)pi * j * W;
+                                src = G.dir + (size_t)par * j * W;
+                                b = dir_bytes;
+                            }
+                        });
             // query direction bits pack(q >= x_parent) (direction.py:53-59)
             for (int pi = 0; pi < gp; pi++)
                 for (int w = 0; w < W; w++) {
@@ -500,34 +747,50 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                     if (lane == 0) qb[pi * W + w] = word;
                 }
             __syncwarp();
-            // matching counts d - popc(dir ^ qbits) (direction.py:62-69)
-            for (int pi = 0; pi < gp; pi++)
-                for (int s = lane; s < j; s += 32) {
-                    int diff = 0;
-                    const uint32_t* dr = drow + ((size_t)pi * j + s) * W;
-                    for (int w = 0; w < W; w++) diff += __popc(dr[w] ^ qb[pi * W + w]);
-                    cnt[pi * j + s] = d - diff;
-                }
-            __syncwarp();
-            // stable argsort(-counts)[:n_keep] (direction.py:79-87)
-            for (int pi = 0; pi < gp; pi++)
-                for (int s = lane; s < j; s += 32) {
-                    int c = cnt[pi * j + s];
-                    int rank = 0;
-                    for (int o = 0; o < j; o++) {
-                        int co = cnt[pi * j + o];
-                        rank += (co > c) || (co == c && o < s);
+            if (j <= 32) {
+                // matching count per slot (lane = slot), then one warp bitonic
+                // sort per parent on (count desc, slot asc) == stable
+                // argsort(-counts) (direction.py:62-87)
+                for (int pi = 0; pi < gp; pi++) {
+                    uint32_t key = 0xFFFFFFFFu;
+                    if ((int)lane < j) {
+                        int diff = 0;
+                        const uint32_t* dr = drow + ((size_t)pi * j + lane) * W;
+                        for (int w = 0; w < W; w++) diff += __popc(dr[w] ^ qb[pi * W + w]);
+                        key = ((uint32_t)(0xFFFF - (d - diff)) << 16) | lane;
                     }
-                    if (rank < nsel) S.cand[(pg + pi) * nsel + rank] = craw[(pg + pi) * j + s];
+                    key = warp_sort_u32(key);
+                    if ((int)lane < nsel)
+                        S.cand[(pg + pi) * nsel + lane] = craw[(pg + pi) * j + (key & 0xFFFFu)];
                 }
+            } else {
+                for (int pi = 0; pi < gp; pi++)
+                    for (int s = lane; s < j; s += 32) {
+                        int diff = 0;
+                        const uint32_t* dr = drow + ((size_t)pi * j + s) * W;
+                        for (int w = 0; w < W; w++) diff += __popc(dr[w] ^ qb[pi * W + w]);
+                        cnt[pi * j + s] = d - diff;
+                    }
+                __syncwarp();
+                for (int pi = 0; pi < gp; pi++)
+                    for (int s = lane; s < j; s += 32) {
+                        int c = cnt[pi * j + s];
+                        int rank = 0;
+                        for (int o = 0; o < j; o++) {
+                            int co = cnt[pi * j + o];
+                            rank += (co > c) || (co == c && o < s);
+                        }
+                        if (rank < nsel) S.cand[(pg + pi) * nsel + rank] = craw[(pg + pi) * j + s];
+                    }
+            }
             __syncwarp();
         }
     } else {
-        for (int pi = 0; pi < np; pi++)
-            warp_copy_async(craw + pi * j, G.adj + (size_t)parents[pi] * j, j * 4);
-        cp_commit();
-        cp_wait<0>();
-        __syncwarp();
+        fetch_group(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
+            dst = craw + r * j;
+            src = G.adj + (size_t)parents[r] * j;
+            b = adj_bytes;
+        });
         for (int pi = 0; pi < np; pi++) {
             if (lane == 0) permutation(rng, (uint32_t)j, perm);  // direction.py:103-105
             __syncwarp();
@@ -542,6 +805,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
 // One full search (search.py:269-335) over graph G.  Seeds (already in
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
+template <int D>
 __device__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                            int ns, bool fill_random, Pcg64& rng, int64_t task,
                            int64_t* n_logged) {
@@ -605,7 +869,7 @@ __device__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, cons
                 *n_logged += n_new;
             }
             S.c_dc += n_new;
-            score_rows(A, S, G, n_new);
+            score_rows<D>(A, S, G, n_new);
             inserted = merge_queue(A, S, C, n_new);
             S.c_ins += inserted;
         }
@@ -629,6 +893,7 @@ __device__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, cons
     return converged;
 }
 
+template <int D>
 __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const unsigned lane = lane_id();
@@ -652,6 +917,11 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
     S.misc = reinterpret_cast<int32_t*>(base + A.o_misc);
     S.gvis = A.gvis + (size_t)gwarp * (A.gmask + 1);
     S.gscr = A.gscratch + (size_t)gwarp * A.gscratch_words;
+    S.mbar = reinterpret_cast<uint64_t*>(base + A.o_mbar);
+    S.phase = 0;
+    if (lane < 3) mbar_init(S.mbar + lane);
+    mbar_fence_init();
+    __syncwarp();
 
     while (true) {
         int task = 0;
@@ -673,7 +943,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         // ghost staging prologue (pipeline.py:218-226)
         if (!has_entry && A.n_seeds == 0 && A.ghost_on) {
             Pcg64 grng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)A.stage));
-            run_search(A, S, A.ghost, A.gcfg, 0, true, grng, task, &n_logged);
+            run_search<D>(A, S, A.ghost, A.gcfg, 0, true, grng, task, &n_logged);
             entry = A.ghost.gid[(uint32_t)S.qk[S.cur][0]];
             has_entry = true;
             g_it = (int32_t)S.c_it;
@@ -705,7 +975,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         __syncwarp();
         Pcg64 rng = A.rng_io ? A.rng_io[task]
                              : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)A.stage));
-        const bool converged = run_search(A, S, G, A.cfg, ns, fill_random, rng, task, &n_logged);
+        const bool converged = run_search<D>(A, S, G, A.cfg, ns, fill_random, rng, task, &n_logged);
         if (A.rng_io && lane == 0) A.rng_io[task] = rng;
 
         // outputs (search.py:323-335, pipeline.py:236-246, :339)
@@ -749,5 +1019,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         __syncwarp();
     }
 }
+
+typedef void (*KernelFn)(KArgs);
 
 }  // namespace pw

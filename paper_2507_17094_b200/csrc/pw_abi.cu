@@ -78,6 +78,29 @@ bool make_plan(int d, L2Plan& P) {
     return P.n_leaves <= kMaxLeaves && P.n_ops <= kMaxOps;
 }
 
+// Dimensions with a compile-time specialisation of K1 (TMA row gathers +
+// compile-time pairwise order); any other d runs the generic instance.
+// (PW_DIMS must match paper_2507_17094_b200/build_ext.py DIMS)
+#define PW_DIMS(X) X(16) X(32) X(64) X(96) X(100) X(128) X(200) X(256) X(384) X(512) X(768) X(960) X(1024)
+typedef KernelFn kernel_fn;
+}  // namespace
+#define PW_DECL(v) KernelFn pw_kernel_##v();
+PW_DIMS(PW_DECL)
+KernelFn pw_kernel_0();
+#undef PW_DECL
+namespace {
+kernel_fn pick_kernel(int d) {
+    switch (d) {
+#define PW_CASE(v) \
+    case v:        \
+        return pw_kernel_##v();
+        PW_DIMS(PW_CASE)
+#undef PW_CASE
+        default:
+            return pw_kernel_0();
+    }
+}
+
 struct DevInfo {
     int sms = 0;
     int smem_optin = 0;
@@ -94,8 +117,13 @@ int dev_info(int dev, DevInfo** out) {
         PW_CUDA(cudaDeviceGetAttribute(&I.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     }
     if (!I.attr_set) {
-        PW_CUDA(cudaFuncSetAttribute(beam_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     I.smem_optin));
+        PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_0(),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+#define PW_ATTR(v)                                                                             \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_##v(),                                 \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+        PW_DIMS(PW_ATTR)
+#undef PW_ATTR
         I.attr_set = true;
     }
     *out = &I;
@@ -251,6 +279,7 @@ struct Launch {
     int warps_per_block = 0;
     int blocks = 0;
     size_t smem = 0;
+    kernel_fn fn = nullptr;
 };
 
 int64_t visit_bound(const SearchCfg& c, int32_t j, int64_t n) {
@@ -309,7 +338,18 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     H = std::max<int64_t>(H, 64);
     A.H = (int32_t)H;
     A.vis_limit = (int32_t)(H * 3 / 4);
-    int R = tun && tun->stage_rows > 0 ? tun->stage_rows : std::max(2, std::min(16, (16384 / (spad * 4)) & ~1));
+    Lc.fn = pick_kernel(d);
+    const bool specialised = Lc.fn != pw_kernel_0();
+    int R;
+    if (tun && tun->stage_rows > 0) {
+        R = tun->stage_rows;
+    } else if (specialised) {
+        // rows in flight per warp: two halves of the staging ring, ~<= 20 KB
+        R = 32;
+        while (R > 4 && (int64_t)R * spad * 4 > 20480) R >>= 1;
+    } else {
+        R = std::max(2, std::min(16, (16384 / (spad * 4)) & ~1));
+    }
     R &= ~1;
     if (R < 2) R = 2;
     int W = sh->W;
@@ -337,7 +377,16 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.o_misc = (int32_t)off;
     int64_t misc = (int64_t)std::max(jm, PG * jm) + (int64_t)PG * W + 8 + p.r + 8;
     off = al(off + 4 * misc);
+    A.o_mbar = (int32_t)off;
+    off = al(off + 3 * 8);
     A.warp_bytes = (int32_t)off;
+    // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
+    auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
+    A.bulk_rows = specialised ? 1 : 0;
+    A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
+                  (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16(4ll * d) && b16(4ll * G.j * W))))
+                     ? 1
+                     : 0;
 
     DevInfo* I;
     if ((rc = dev_info(sh->device, &I))) return rc;
@@ -398,7 +447,9 @@ int launch(pw_shard* sh, Launch& Lc, cudaStream_t st) {
     PW_CUDA(cudaSetDevice(sh->device));
     PW_CUDA(cudaMemsetAsync(sh->counter, 0, sizeof(int32_t), st));  // task counter only; err sticks
     int blocks = std::min<int64_t>(Lc.blocks, ((int64_t)Lc.A.n_tasks + Lc.warps_per_block - 1) / Lc.warps_per_block);
-    beam_search_kernel<<<blocks, 32 * Lc.warps_per_block, Lc.smem, st>>>(Lc.A);
+    void* args[] = {(void*)&Lc.A};
+    PW_CUDA(cudaLaunchKernel((const void*)Lc.fn, dim3(blocks), dim3(32 * Lc.warps_per_block), args,
+                             Lc.smem, st));
     g_launches++;
     PW_CUDA(cudaGetLastError());
     return 0;
