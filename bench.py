@@ -190,7 +190,8 @@ def run_ours(args, cfg):
     truth = ground_truth(W, cfg["k"]) if rank == 0 else None
     queries = W["queries"]
     nq, k = queries.shape[0], cfg["k"]
-    eng = ring.RingSearch(shard, nq, k, rank, world, dev)
+    tuning = json.loads(args.tuning) if args.tuning else None
+    eng = ring.RingSearch(shard, nq, k, rank, world, dev, tuning=tuning)
 
     def search(params, mode, timer=None):
         return eng.run(queries, params, mode, timer=timer)
@@ -308,7 +309,7 @@ def run_ours(args, cfg):
                        "arm": "pipelined path extension + ghost staging (rho=0.01) + direction-guided"
                               " selection (discard 0.5, cooldown 0.3)",
                        "l": ops["pathweaver"]["l"], "recall_at_10": ops["pathweaver"]["recall"],
-                       "m": 64, "r": 8, "max_iter": 64,
+                       "m": 64, "r": 8, "max_iter": 64, "tuning": tuning,
                        "l2_policy": "inputs larger than L2 (vectors %.2f GB + graph/direction %.2f GB "
                                     "per shard, random row gathers)" % (
                                         W["vec"].numel() * 4 / 1e9,
@@ -455,6 +456,8 @@ def main():
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--tuning", default=os.environ.get("PW_TUNING", ""),
+                    help='JSON device knobs, e.g. {"stage_rows": 16, "row_copy": 1}')
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

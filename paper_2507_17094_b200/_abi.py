@@ -11,7 +11,7 @@ import os
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libpwb200.so"
+LIB_PATH = Path(os.environ["PW_LIB"]) if os.environ.get("PW_LIB") else _PKG / "libpwb200.so"
 
 PW_OK, PW_EINVAL, PW_ENOMEM, PW_ECUDA = 0, -1, -2, -3
 SELECTION = {"full": 0, "direction": 1, "random": 2}
@@ -31,7 +31,7 @@ class Params(C.Structure):
 
 class Tuning(C.Structure):
     _fields_ = [("visited_slots", C.c_int32), ("stage_rows", C.c_int32),
-                ("warps_per_sm", C.c_int32)]
+                ("warps_per_sm", C.c_int32), ("row_copy", C.c_int32)]
 
 
 class ShardDesc(C.Structure):
@@ -131,6 +131,6 @@ def params_struct(p) -> Params:
 
 def tuning_struct(t) -> Tuning:
     if t is None:
-        return Tuning(0, 0, 0)
+        return Tuning(0, 0, 0, 0)
     return Tuning(int(t.get("visited_slots", 0)), int(t.get("stage_rows", 0)),
-                  int(t.get("warps_per_sm", 0)))
+                  int(t.get("warps_per_sm", 0)), int(t.get("row_copy", 0)))

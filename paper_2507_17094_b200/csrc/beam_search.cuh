@@ -304,8 +304,10 @@ __device__ __forceinline__ float pw_sum(const float* x, const float* q, unsigned
 // --------------------------------------------------------------- per warp
 struct WarpState {
     float* q;
-    uint64_t* qk[2];
-    uint8_t* qe[2];
+    uint64_t* qk0;
+    uint64_t* qk1;
+    uint8_t* qe0;
+    uint8_t* qe1;
     int32_t* cand;
     int32_t* cslot;
     int32_t* newl;
@@ -320,6 +322,10 @@ struct WarpState {
     uint64_t* mbar;         // [0],[1] gather halves, [2] expansion fetch
     uint32_t phase;         // parity bit per mbarrier
     int32_t cur;            // current queue buffer
+    __device__ __forceinline__ uint64_t* qk_cur() const { return cur ? qk1 : qk0; }
+    __device__ __forceinline__ uint64_t* qk_nxt() const { return cur ? qk0 : qk1; }
+    __device__ __forceinline__ uint8_t* qe_cur() const { return cur ? qe1 : qe0; }
+    __device__ __forceinline__ uint8_t* qe_nxt() const { return cur ? qe0 : qe1; }
     int32_t qlen;
     int32_t vcount;         // entries in the smem visited table
     bool ovf;               // visited set spilled to the global table
@@ -453,26 +459,46 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
     const int ngroups = (n + RH - 1) / RH;
     if constexpr (D > 0) {
         constexpr uint32_t row_bytes = D * 4;
+        constexpr int CPR = D / 4;  // 16-byte chunks per row
+        const bool tma = A.bulk_rows != 0;
         auto issue = [&](int g) {
-            if (g >= ngroups) return;
+            if (g >= ngroups) {
+                if (!tma) cp_commit();
+                return;
+            }
             const int r0 = g * RH;
             const int rows = min(RH, n - r0);
             float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
-            uint64_t* bar = S.mbar + (g & 1);
-            fence_proxy_async();
-            if (lane == 0) mbar_arrive_expect(bar, rows * row_bytes);
-            __syncwarp();
-            for (int r = lane; r < rows; r += 32) {
-                const int32_t id = S.newl[r0 + r];
-                bulk_g2s(dst0 + (size_t)r * sp, G.vec + (size_t)id * D, row_bytes, bar);
+            if (tma) {
+                uint64_t* bar = S.mbar + (g & 1);
+                fence_proxy_async();
+                if (lane == 0) mbar_arrive_expect(bar, rows * row_bytes);
+                __syncwarp();
+                for (int r = lane; r < rows; r += 32) {
+                    const int32_t id = S.newl[r0 + r];
+                    bulk_g2s(dst0 + (size_t)r * sp, G.vec + (size_t)id * D, row_bytes, bar);
+                }
+            } else {
+                // LDGSTS: 16-byte chunks of all rows of the half, lane-strided
+                for (int c = lane; c < rows * CPR; c += 32) {
+                    const int r = c / CPR, ch = c - r * CPR;
+                    const int32_t id = S.newl[r0 + r];
+                    cp_async16(dst0 + (size_t)r * sp + 4 * ch, G.vec + (size_t)id * D + 4 * ch);
+                }
+                cp_commit();
             }
         };
         issue(0);
         issue(1);
         const unsigned v = lane >> 1, h = lane & 1u;
         for (int g = 0; g < ngroups; g++) {
-            mbar_wait(S.mbar + (g & 1), (S.phase >> (g & 1)) & 1u);
-            S.phase ^= 1u << (g & 1);
+            if (tma) {
+                mbar_wait(S.mbar + (g & 1), (S.phase >> (g & 1)) & 1u);
+                S.phase ^= 1u << (g & 1);
+            } else {
+                cp_wait<1>();
+                __syncwarp();
+            }
             const int r0 = g * RH;
             const int rows = min(RH, n - r0);
             const float* base = S.stage + (size_t)(g & 1) * RH * sp;
@@ -488,6 +514,7 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
             __syncwarp();
             issue(g + 2);
         }
+        if (!tma) cp_wait<0>();
         __syncwarp();
     } else {
         const int row_bytes = A.d * 4;
@@ -529,14 +556,40 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
     }
 }
 
+// Bitonic sort of ckey[0..s) in shared memory (32 < s <= 256): compact
+// loops (this case only occurs in the first iterations of a search, so code
+// size matters more than its instruction count).
+static __device__ __noinline__ void sort_survivors_smem(WarpState& S, int s) {
+    const unsigned lane = lane_id();
+    int N = 64;
+    while (N < s) N <<= 1;
+    for (int e = s + (int)lane; e < N; e += 32) S.ckey[e] = ~0ull;
+    __syncwarp();
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = lane; i < (N >> 1); i += 32) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool asc = (lo & size) == 0;
+                const uint64_t a = S.ckey[lo], b = S.ckey[hi];
+                if ((a > b) == asc) {
+                    S.ckey[lo] = b;
+                    S.ckey[hi] = a;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // search.py:170-190 merge_and_sort on keys; returns `inserted`.
 static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int n) {
     const unsigned lane = lane_id();
     const int L = C.L;
-    const uint64_t* qk = S.qk[S.cur];
-    const uint8_t* qe = S.qe[S.cur];
-    uint64_t* nk = S.qk[S.cur ^ 1];
-    uint8_t* ne = S.qe[S.cur ^ 1];
+    const uint64_t* qk = S.qk_cur();
+    const uint8_t* qe = S.qe_cur();
+    uint64_t* nk = S.qk_nxt();
+    uint8_t* ne = S.qe_nxt();
     const int qlen = S.qlen;
     const uint64_t thr = qlen == L ? qk[L - 1] : ~0ull;
     // survivors (compacted in place in ckey)
@@ -552,11 +605,16 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     }
     __syncwarp();
     if (s == 0) return 0;
-    if (s <= 32) {
-        // bitonic-sort the survivors across the warp, then merge-path positions
-        uint64_t mine = (int)lane < s ? S.ckey[lane] : ~0ull;
-        mine = warp_sort_u64(mine);
-        if ((int)lane < s) S.ckey[lane] = mine;
+    if (s <= 256) {
+        // sort the survivors (warp bitonic, K per lane) into ckey[0..s), then
+        // merge-path positions by binary search on both sorted runs
+        if (s <= 32) {
+            uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
+            x = warp_sort_u64(x);
+            if ((int)lane < s) S.ckey[lane] = x;
+        } else {
+            sort_survivors_smem(S, s);
+        }
         __syncwarp();
         for (int t = lane; t < qlen; t += 32) {
             const uint64_t key = qk[t];
@@ -572,22 +630,27 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
                 ne[np] = qe[t];
             }
         }
-        bool kept = false;
-        if ((int)lane < s) {
-            int lo = 0, hi = qlen;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (qk[mid] < mine) lo = mid + 1;
-                else hi = mid;
+        int ins = 0;
+        for (int base = 0; base < s; base += 32) {
+            const int i = base + (int)lane;
+            bool kept = false;
+            if (i < s) {
+                const uint64_t mine = S.ckey[i];
+                int lo = 0, hi = qlen;
+                while (lo < hi) {
+                    int mid = (lo + hi) >> 1;
+                    if (qk[mid] < mine) lo = mid + 1;
+                    else hi = mid;
+                }
+                const int p = i + lo;
+                if (p < L) {
+                    nk[p] = mine;
+                    ne[p] = 0;
+                    kept = true;
+                }
             }
-            const int p = (int)lane + lo;
-            if (p < L) {
-                nk[p] = mine;
-                ne[p] = 0;
-                kept = true;
-            }
+            ins += __popc(__ballot_sync(0xffffffffu, kept));
         }
-        const int ins = __popc(__ballot_sync(0xffffffffu, kept));
         __syncwarp();
         S.qlen = min(L, qlen + s);
         S.cur ^= 1;
@@ -637,8 +700,8 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
 // search.py:192-204: first r unexpanded queue entries, marked expanded.
 static __device__ int select_parents(WarpState& S, int r, int32_t* parents) {
     const unsigned lane = lane_id();
-    uint64_t* qk = S.qk[S.cur];
-    uint8_t* qe = S.qe[S.cur];
+    uint64_t* qk = S.qk_cur();
+    uint8_t* qe = S.qe_cur();
     int np = 0;
     for (int base = 0; base < S.qlen && np < r; base += 32) {
         int t = base + lane;
@@ -693,7 +756,8 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
 
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
 // returns the candidate count p * n_sel.
-static __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
+template <int D>
+__device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                       const int32_t* parents, int np, int it, Pcg64& rng) {
     const unsigned lane = lane_id();
     const int j = G.j;
@@ -714,7 +778,9 @@ static __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, co
     int32_t* perm = S.misc;                               // j (random arm)
     uint32_t* qb = reinterpret_cast<uint32_t*>(S.misc + A.PG * j);  // PG * W
     if (C.prune_sel == 1) {
-        const int W = A.W, d = A.d;
+        constexpr int WC = D > 0 ? (D + 31) / 32 : 0;
+        const int W = WC ? WC : A.W;
+        const int d = D > 0 ? D : A.d;
         const uint32_t vec_bytes = (uint32_t)d * 4u, dir_bytes = (uint32_t)(j * W) * 4u;
         for (int pg = 0; pg < np; pg += A.PG) {
             const int gp = min(A.PG, np - pg);
@@ -738,25 +804,34 @@ static __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, co
                                 b = dir_bytes;
                             }
                         });
-            // query direction bits pack(q >= x_parent) (direction.py:53-59)
-            for (int pi = 0; pi < gp; pi++)
-                for (int w = 0; w < W; w++) {
-                    int t = 32 * w + (int)lane;
-                    bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
-                    unsigned word = __ballot_sync(0xffffffffu, bit);
-                    if (lane == 0) qb[pi * W + w] = word;
-                }
-            __syncwarp();
-            if (j <= 32) {
-                // matching count per slot (lane = slot), then one warp bitonic
-                // sort per parent on (count desc, slot asc) == stable
-                // argsort(-counts) (direction.py:62-87)
+            if (WC > 0 && j <= 32) {
+                // per parent: query direction bits pack(q >= x_parent) as W
+                // ballots (direction.py:53-59), matching count per slot
+                // (lane = slot, :62-69), one warp bitonic sort on (count desc,
+                // slot asc) == stable argsort(-counts) (:79-87)
                 for (int pi = 0; pi < gp; pi++) {
+                    uint32_t qb[WC > 0 ? WC : 1];
+#pragma unroll
+                    for (int w = 0; w < WC; w++) {
+                        const int t = 32 * w + (int)lane;
+                        const bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
+                        qb[w] = __ballot_sync(0xffffffffu, bit);
+                    }
                     uint32_t key = 0xFFFFFFFFu;
                     if ((int)lane < j) {
+                        const uint32_t* dr = drow + ((size_t)pi * j + lane) * WC;
                         int diff = 0;
-                        const uint32_t* dr = drow + ((size_t)pi * j + lane) * W;
-                        for (int w = 0; w < W; w++) diff += __popc(dr[w] ^ qb[pi * W + w]);
+                        if constexpr (WC % 4 == 0) {
+#pragma unroll
+                            for (int w = 0; w < WC; w += 4) {
+                                const uint4 v = *reinterpret_cast<const uint4*>(dr + w);
+                                diff += __popc(v.x ^ qb[w]) + __popc(v.y ^ qb[w + 1]) +
+                                        __popc(v.z ^ qb[w + 2]) + __popc(v.w ^ qb[w + 3]);
+                            }
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < WC; w++) diff += __popc(dr[w] ^ qb[w]);
+                        }
                         key = ((uint32_t)(0xFFFF - (d - diff)) << 16) | lane;
                     }
                     key = warp_sort_u32(key);
@@ -764,6 +839,14 @@ static __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, co
                         S.cand[(pg + pi) * nsel + lane] = craw[(pg + pi) * j + (key & 0xFFFFu)];
                 }
             } else {
+                for (int pi = 0; pi < gp; pi++)
+                    for (int w = 0; w < W; w++) {
+                        int t = 32 * w + (int)lane;
+                        bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
+                        unsigned word = __ballot_sync(0xffffffffu, bit);
+                        if (lane == 0) qb[pi * W + w] = word;
+                    }
+                __syncwarp();
                 for (int pi = 0; pi < gp; pi++)
                     for (int s = lane; s < j; s += 32) {
                         int diff = 0;
@@ -806,7 +889,7 @@ static __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, co
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
 template <int D>
-__device__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
+__device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                            int ns, bool fill_random, Pcg64& rng, int64_t task,
                            int64_t* n_logged) {
     const unsigned lane = lane_id();
@@ -884,7 +967,7 @@ __device__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, cons
             break;
         }
         S.c_ne += np;
-        int nc = expand(A, S, G, C, parents, np, it, rng);
+        int nc = expand<D>(A, S, G, C, parents, np, it, rng);
         nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
         S.c_tv += nb;
         bh_clear(A, S);
@@ -902,10 +985,10 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
     unsigned char* base = smem_raw + (size_t)warp * A.warp_bytes;
     WarpState S;
     S.q = reinterpret_cast<float*>(base + A.o_q);
-    S.qk[0] = reinterpret_cast<uint64_t*>(base + A.o_qk);
-    S.qk[1] = S.qk[0] + A.L_max;
-    S.qe[0] = reinterpret_cast<uint8_t*>(base + A.o_qe);
-    S.qe[1] = S.qe[0] + A.L_max;
+    S.qk0 = reinterpret_cast<uint64_t*>(base + A.o_qk);
+    S.qk1 = S.qk0 + A.L_max;
+    S.qe0 = reinterpret_cast<uint8_t*>(base + A.o_qe);
+    S.qe1 = S.qe0 + A.L_max;
     S.cand = reinterpret_cast<int32_t*>(base + A.o_cand);
     S.cslot = reinterpret_cast<int32_t*>(base + A.o_cslot);
     S.newl = reinterpret_cast<int32_t*>(base + A.o_newl);
@@ -940,46 +1023,54 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         int32_t entry = has_entry ? A.entries[task] : -1;
         const GraphDev& G = A.use_ghost_graph ? A.ghost : A.main;
 
-        // ghost staging prologue (pipeline.py:218-226)
-        if (!has_entry && A.n_seeds == 0 && A.ghost_on) {
-            Pcg64 grng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)A.stage));
-            run_search<D>(A, S, A.ghost, A.gcfg, 0, true, grng, task, &n_logged);
-            entry = A.ghost.gid[(uint32_t)S.qk[S.cur][0]];
-            has_entry = true;
-            g_it = (int32_t)S.c_it;
-            g_dc = S.c_dc;
-            g_tv = S.c_tv;
-            g_ne = S.c_ne;
-            n_logged = 0;
-        }
-        // seeds (pipeline.py:227-231, search.py:294)
-        int ns = 0;
-        bool fill_random;
-        if (A.n_seeds > 0) {
-            for (int t = lane; t < A.n_seeds; t += 32) S.cand[t] = (int32_t)A.seeds[t];
-            ns = A.n_seeds;
-            fill_random = A.seed_mode == 1;
-        } else if (has_entry) {
-            if (lane == 0) S.cand[0] = entry;
-            ns = 1;
-            if (A.seed_mode == 0) {
-                for (int t = lane; t < G.j; t += 32) S.cand[1 + t] = G.adj[(size_t)entry * G.j + t];
-                ns = 1 + G.j;
-                fill_random = false;
+        // Phase 0 = ghost staging (pipeline.py:218-226) when the task has no
+        // entry; phase 1 = the shard search.  One call site keeps a single
+        // inlined copy of run_search in the kernel.
+        bool converged = false;
+        const bool ghost_phase = !has_entry && A.n_seeds == 0 && A.ghost_on;
+        for (int phase = ghost_phase ? 0 : 1; phase < 2; phase++) {
+            const bool gph = phase == 0;
+            int ns = 0;
+            bool fill_random = true;
+            Pcg64 rng;
+            if (gph) {
+                rng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)A.stage));
             } else {
-                fill_random = true;
+                // seeds (pipeline.py:227-231, search.py:294)
+                if (A.n_seeds > 0) {
+                    for (int t = lane; t < A.n_seeds; t += 32) S.cand[t] = (int32_t)A.seeds[t];
+                    ns = A.n_seeds;
+                    fill_random = A.seed_mode == 1;
+                } else if (has_entry) {
+                    if (lane == 0) S.cand[0] = entry;
+                    ns = 1;
+                    if (A.seed_mode == 0) {
+                        for (int t = lane; t < G.j; t += 32) S.cand[1 + t] = G.adj[(size_t)entry * G.j + t];
+                        ns = 1 + G.j;
+                        fill_random = false;
+                    }
+                }
+                __syncwarp();
+                rng = A.rng_io ? A.rng_io[task]
+                               : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)A.stage));
             }
-        } else {
-            fill_random = true;
+            converged = run_search<D>(A, S, gph ? A.ghost : G, gph ? A.gcfg : A.cfg, ns, fill_random,
+                                      rng, task, &n_logged);
+            if (gph) {
+                entry = A.ghost.gid[(uint32_t)S.qk_cur()[0]];
+                has_entry = true;
+                g_it = (int32_t)S.c_it;
+                g_dc = S.c_dc;
+                g_tv = S.c_tv;
+                g_ne = S.c_ne;
+                n_logged = 0;
+            } else if (A.rng_io && lane == 0) {
+                A.rng_io[task] = rng;
+            }
         }
-        __syncwarp();
-        Pcg64 rng = A.rng_io ? A.rng_io[task]
-                             : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)A.stage));
-        const bool converged = run_search<D>(A, S, G, A.cfg, ns, fill_random, rng, task, &n_logged);
-        if (A.rng_io && lane == 0) A.rng_io[task] = rng;
 
         // outputs (search.py:323-335, pipeline.py:236-246, :339)
-        const uint64_t* qk = S.qk[S.cur];
+        const uint64_t* qk = S.qk_cur();
         const int nk = min(S.qlen, A.cfg.k);
         for (int t = lane; t < nk; t += 32) {
             uint64_t key = qk[t];

@@ -369,7 +369,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.o_cand = (int32_t)off; off = al(off + 4 * cb);
     A.o_cslot = (int32_t)off; off = al(off + 4 * cb);
     A.o_newl = (int32_t)off; off = al(off + 4 * cb);
-    A.o_ckey = (int32_t)off; off = al(off + 8 * cb);
+    A.o_ckey = (int32_t)off; off = al(off + 8 * std::max<int64_t>(64, next_pow2(cb)));  // pow2 for the survivor sort
     A.o_bhk = (int32_t)off; off = al(off + 4 * (int64_t)A.BH);
     A.o_bhp = (int32_t)off; off = al(off + 4 * (int64_t)A.BH);
     A.o_vh = (int32_t)off; off = al(off + 4 * H);
@@ -382,7 +382,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.warp_bytes = (int32_t)off;
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
-    A.bulk_rows = specialised ? 1 : 0;
+    A.bulk_rows = (specialised && tun && tun->row_copy == 1) ? 1 : 0;
     A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
                   (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16(4ll * d) && b16(4ll * G.j * W))))
                      ? 1

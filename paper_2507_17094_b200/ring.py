@@ -66,12 +66,13 @@ def run_ring_pipelined(stage_fn, q: int, rank: int, world: int, send_recv, on_st
 class RingSearch:
     """Device engine of one rank (one shard on this GPU)."""
 
-    def __init__(self, shard, q: int, k: int, rank: int, world: int, device):
+    def __init__(self, shard, q: int, k: int, rank: int, world: int, device, tuning=None):
         import torch
 
         from . import device as dv
 
         self.shard, self.q, self.k, self.rank, self.world = shard, q, k, rank, world
+        self.tuning = tuning
         self.dev = torch.device(device)
         self.run_buf = dv.DeviceRun(q, world, k, self.dev)
         self.stream = torch.cuda.current_stream(self.dev)
@@ -87,7 +88,8 @@ class RingSearch:
 
         R = self.run_buf
         if self.world == 1:
-            dv.run_local([self.shard], params, queries, mode, R, stream=self.stream, timer=timer)
+            dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning,
+                         stream=self.stream, timer=timer)
             return R.final_ids.cpu().numpy()
 
         R.reset()
@@ -99,7 +101,8 @@ class RingSearch:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(self.stream)
             dv.search_stage(self.shard, params, queries, q0, n, stage, R, g, stage,
-                            entries_in=entries_in, forward_out=forward_out, stream=self.stream)
+                            entries_in=entries_in, forward_out=forward_out, tuning=self.tuning,
+                            stream=self.stream)
             if timer is not None:
                 e1.record(self.stream)
                 timer.append((e0, e1))
@@ -154,7 +157,7 @@ class RingSearch:
                        comm=np.empty((1, 1), np.int64))
             handles = (C.c_void_p * 1)(self.shard.handle.value)
             p = _abi.params_struct(params)
-            t = _abi.tuning_struct(None)
+            t = _abi.tuning_struct(self.tuning)
             _abi.check(lib.pw_run(handles, 1, C.byref(p), C.byref(t), queries_host.ctypes.data, q,
                                   _abi.MODE["pipelined"], out["shard_ids"].ctypes.data,
                                   out["shard_dists"].ctypes.data, out["final_ids"].ctypes.data,

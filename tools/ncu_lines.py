@@ -39,3 +39,30 @@ print("stall reasons:", ", ".join(f"{k[6:]} {v / ts * 100:.1f}%" for k, v in sor
 for o in sorted(out, key=lambda o: -o[1])[:top]:
     main = max(o[4].items(), key=lambda kv: kv[1])[0][6:] if o[4] else ""
     print(f"{o[0] / ti * 100:5.1f}% inst {o[1] / ts * 100:5.1f}% stall ({main:12s}) L{o[2]:4d} {o[3]}")
+
+# per-function aggregation (functions located by scanning the source file)
+import re
+from pathlib import Path
+src = Path(__file__).resolve().parent.parent / "paper_2507_17094_b200" / "csrc" / "beam_search.cuh"
+lines = src.read_text().splitlines()
+starts = []
+for i, l in enumerate(lines, 1):
+    m = re.match(r"^(?:template <[^>]*>\s*)?(?:static\s+)?(?:__device__|__global__)[^(]*?\b(\w+)\s*\(", l)
+    if m:
+        starts.append((i, m.group(1)))
+starts.sort()
+def fn_of(line):
+    name = "?"
+    for s, n in starts:
+        if s <= line:
+            name = n
+    return name
+by = {}
+for o in out:
+    f = fn_of(o[2])
+    a = by.setdefault(f, [0, 0])
+    a[0] += o[0]
+    a[1] += o[1]
+print("\nper function (inst %, stall %):")
+for f, (i_, s_) in sorted(by.items(), key=lambda kv: -kv[1][1])[:20]:
+    print(f"  {f:22s} {i_ / ti * 100:5.1f}% {s_ / ts * 100:5.1f}%")
