@@ -170,6 +170,13 @@ int pw_run_device(pw_shard* const* shards, int32_t n_shards, const pw_params* pa
 int pw_squared_l2_rows(pw_shard* shard, const int32_t* ids, int64_t n_ids,
                        const float* query, float* out, void* stream);
 
+/* Launch configuration K1 would use for (shard, params, tuning) without
+ * launching: out[0] warps per CTA (= resident query-warps per SM), out[1]
+ * shared-memory bytes per warp, out[2] visited-table slots, out[3] staging
+ * rows, out[4] specialised dimension (0 = generic), out[5] blocks. */
+int pw_launch_config(pw_shard* shard, const pw_params* params, const pw_tuning* tuning,
+                     int32_t* out6);
+
 /* Number of kernel launches issued by this library since load (evidence for
  * bench.py's gpu_launches). */
 int64_t pw_launch_count(void);

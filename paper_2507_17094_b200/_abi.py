@@ -80,6 +80,7 @@ EXPORTS = {
                                 C.c_void_p, C.c_int64, C.c_int32] + [C.c_void_p] * 9),
     "pw_squared_l2_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p]),
+    "pw_launch_config": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(Tuning), C.c_void_p]),
 }
 
 _LIB = None
@@ -134,3 +135,14 @@ def tuning_struct(t) -> Tuning:
         return Tuning(0, 0, 0, 0)
     return Tuning(int(t.get("visited_slots", 0)), int(t.get("stage_rows", 0)),
                   int(t.get("warps_per_sm", 0)), int(t.get("row_copy", 0)))
+
+
+def launch_config(shard_handle, params, tuning=None) -> dict:
+    """K1 launch configuration for a shard/params/tuning (no launch)."""
+    lib = load()
+    out = (C.c_int32 * 6)()
+    p = params_struct(params)
+    t = tuning_struct(tuning)
+    check(lib.pw_launch_config(shard_handle, C.byref(p), C.byref(t), out))
+    return dict(warps_per_sm=out[0], smem_per_warp=out[1], visited_slots=out[2], stage_rows=out[3],
+                specialised_d=out[4], blocks=out[5])

@@ -94,12 +94,13 @@ struct KArgs {
     // per-warp shared-memory layout (bytes)
     int32_t L_max, CB, BH, H, R, PG;
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
-        o_misc, o_mbar, warp_bytes;
+        o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
     int32_t bulk_adj;       // adjacency / direction rows may use cp.async.bulk
     int32_t vis_limit;      // smem visited entries before spilling to global
-    uint32_t* gvis;         // per-warp global visited tables
+    unsigned long long* gvis;  // per-warp global visited spill tables, (epoch << 32 | id)
     int32_t gmask;
+    uint32_t* gepoch;       // per-warp search epoch (tags the spill table; no clearing)
     uint32_t* gscratch;     // per-warp global scratch for choice()
     int64_t gscratch_words;
     int32_t* task_counter;
@@ -289,6 +290,50 @@ __device__ __forceinline__ float pw_leaf(const float* x, const float* q, unsigne
     }
 }
 
+// Same order with 4 lanes per row (8 rows per warp pass): lane c = lane&3
+// owns accumulators 2c, 2c+1 (one float2 per 8-element step); the xor-1 and
+// xor-2 shuffles form ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)).
+template <int OFF, int N>
+__device__ __forceinline__ float pw_leaf4(const float* x, const float* q, unsigned c) {
+    if constexpr (N < 8) {
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
+        return s;
+    } else {
+        constexpr int NF = N - (N % 8);
+        const float2* x2 = reinterpret_cast<const float2*>(x + OFF);
+        const float2* q2 = reinterpret_cast<const float2*>(q + OFF);
+        float2 xv = x2[c], qv = q2[c];
+        float r0 = sqd(xv.x, qv.x), r1 = sqd(xv.y, qv.y);
+#pragma unroll
+        for (int p = 1; p < NF / 8; p++) {
+            xv = x2[4 * p + c];
+            qv = q2[4 * p + c];
+            r0 = __fadd_rn(r0, sqd(xv.x, qv.x));
+            r1 = __fadd_rn(r1, sqd(xv.y, qv.y));
+        }
+        float a = __fadd_rn(r0, r1);
+        a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+        float s = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
+#pragma unroll
+        for (int i = NF; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
+        return s;
+    }
+}
+
+template <int OFF, int N>
+__device__ __forceinline__ float pw_sum4(const float* x, const float* q, unsigned c) {
+    if constexpr (N <= 128) {
+        return pw_leaf4<OFF, N>(x, q, c);
+    } else {
+        constexpr int N2 = N / 2 - (N / 2) % 8;
+        float a = pw_sum4<OFF, N2>(x, q, c);
+        float b = pw_sum4<OFF + N2, N - N2>(x, q, c);
+        return __fadd_rn(a, b);
+    }
+}
+
 template <int OFF, int N>
 __device__ __forceinline__ float pw_sum(const float* x, const float* q, unsigned h) {
     if constexpr (N <= 128) {
@@ -317,9 +362,11 @@ struct WarpState {
     uint32_t* vh;
     float* stage;
     int32_t* misc;
-    uint32_t* gvis;
+    unsigned long long* gvis;
     uint32_t* gscr;
+    uint32_t epoch;         // this search's spill-table tag (0 never used)
     uint64_t* mbar;         // [0],[1] gather halves, [2] expansion fetch
+    uint4* desc;            // bulk-copy descriptors of one expansion fetch (<= 32)
     uint32_t phase;         // parity bit per mbarrier
     int32_t cur;            // current queue buffer
     __device__ __forceinline__ uint64_t* qk_cur() const { return cur ? qk1 : qk0; }
@@ -357,9 +404,14 @@ __device__ __forceinline__ bool bh_contains(const KArgs& A, const WarpState& S, 
 }
 
 __device__ __forceinline__ void bh_clear(const KArgs& A, WarpState& S) {
-    for (int i = lane_id(); i < A.BH; i += 32) {
-        S.bhk[i] = kEmpty;
-        S.bhp[i] = 0x7FFFFFFF;
+    uint4* k4 = reinterpret_cast<uint4*>(S.bhk);
+    uint4* p4 = reinterpret_cast<uint4*>(S.bhp);
+    const uint4 e = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    const uint4 m = make_uint4(0x7FFFFFFFu, 0x7FFFFFFFu, 0x7FFFFFFFu, 0x7FFFFFFFu);
+#pragma unroll 1
+    for (int i = lane_id(); i < (A.BH >> 2); i += 32) {
+        k4[i] = e;
+        p4[i] = m;
     }
     __syncwarp();
 }
@@ -411,38 +463,135 @@ __device__ __forceinline__ bool visit_insert(const KArgs& A, WarpState& S, uint3
         atomicOr(A.err, 4);  // smem visited table full: impossible below vis_limit
         return false;
     }
+    // spilled: per-warp global table whose entries carry the search epoch, so
+    // stale entries of earlier searches read as empty and nothing is cleared
     const uint32_t gm = (uint32_t)A.gmask;
+    const unsigned long long want = ((unsigned long long)S.epoch << 32) | id;
     uint32_t g = (hash32(id ^ 0x5bd1e995u) >> 3) & gm;
-    for (uint32_t gp = 0; gp <= gm; gp++) {
-        uint32_t old = atomicCAS(&S.gvis[g], kEmpty, id);
-        if (old == kEmpty) return true;
-        if (old == id) return false;
+    for (uint32_t gp = 0; gp <= gm;) {
+        unsigned long long v = S.gvis[g];
+        if (v == want) return false;
+        if ((uint32_t)(v >> 32) != S.epoch) {
+            unsigned long long old = atomicCAS(&S.gvis[g], v, want);
+            if (old == v) return true;
+            if (old == want) return false;
+            continue;  // slot changed under us: re-examine it
+        }
         g = (g + 1u) & gm;
+        gp++;
     }
     atomicOr(A.err, 8);  // global visited table full
     return false;
 }
 
+__device__ __forceinline__ bool smem_lookup(const KArgs& A, const WarpState& S, uint32_t id) {
+    const uint32_t hm = (uint32_t)A.H - 1u;
+    uint32_t h = hash32(id) & hm;
+    for (int probe = 0; probe <= A.H; probe++) {
+        const uint32_t v = S.vh[h];
+        if (v == id) return true;
+        if (v == kEmpty) return false;
+        h = (h + 1u) & hm;
+    }
+    return false;
+}
+
+// Linear-probing insert-if-absent into the epoch-tagged spill table, starting
+// at slot g whose current content is cur (the rare collision path).
+static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint32_t gm, uint32_t epoch,
+                                                 uint32_t id, uint32_t g, unsigned long long cur,
+                                                 int32_t* err) {
+    const unsigned long long want = ((unsigned long long)epoch << 32) | id;
+    for (uint32_t gp = 0; gp <= gm;) {
+        if (cur == want) return false;
+        if ((uint32_t)(cur >> 32) != epoch) {
+            const unsigned long long o = atomicCAS(&gvis[g], cur, want);
+            if (o == cur) return true;
+            cur = o;
+            continue;
+        }
+        g = (g + 1u) & gm;
+        gp++;
+        cur = gvis[g];
+    }
+    atomicOr(err, 8);  // global visited table full
+    return false;
+}
+
 // Keep only never-scored ids of newl[0..nb) (in order); returns n_new.
+// Until the shared-memory table would pass vis_limit, inserts go there
+// (one CAS each, no global traffic).  After the spill, every candidate not in
+// the (now read-only) shared table is resolved against the per-warp global
+// epoch table with all of a lane's probes in flight at once: first-slot
+// loads, then CASes, then (rarely) linear-probing retries.
 static __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
     const unsigned lane = lane_id();
-    if (!S.ovf && S.vcount + nb > A.vis_limit) {
-        S.ovf = true;
-        for (int i = lane; i <= A.gmask; i += 32) S.gvis[i] = kEmpty;
-        __syncwarp();
-    }
+    if (!S.ovf && S.vcount + nb > A.vis_limit) S.ovf = true;
     int cnt = 0;
-    for (int base = 0; base < nb; base += 32) {
-        int t = base + lane;
-        int32_t id = t < nb ? S.newl[t] : -1;
-        bool f = t < nb && visit_insert(A, S, (uint32_t)id);
-        unsigned b = __ballot_sync(0xffffffffu, f);
-        int pos = cnt + __popc(b & lanemask_lt());
-        if (f) S.newl[pos] = id;
-        cnt += __popc(b);
+    if (!S.ovf) {
+        for (int base = 0; base < nb; base += 32) {
+            int t = base + lane;
+            int32_t id = t < nb ? S.newl[t] : -1;
+            bool f = t < nb && visit_insert(A, S, (uint32_t)id);
+            unsigned b = __ballot_sync(0xffffffffu, f);
+            int pos = cnt + __popc(b & lanemask_lt());
+            if (f) S.newl[pos] = id;
+            cnt += __popc(b);
+        }
+        __syncwarp();
+        S.vcount += cnt;
+        return cnt;
+    }
+    constexpr int K = 8;
+    const uint32_t gm = (uint32_t)A.gmask;
+    for (int base0 = 0; base0 < nb; base0 += 32 * K) {
+        int32_t id[K];
+        uint32_t slot[K];
+        unsigned long long v[K];
+        bool pend[K], fresh[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int t = base0 + k * 32 + (int)lane;
+            id[k] = t < nb ? S.newl[t] : -1;
+            pend[k] = t < nb && !smem_lookup(A, S, (uint32_t)id[k]);
+            slot[k] = (hash32((uint32_t)id[k] ^ 0x5bd1e995u) >> 3) & gm;
+            v[k] = pend[k] ? S.gvis[slot[k]] : 0ull;
+            fresh[k] = false;
+        }
+        // one CAS per stale first slot, all in flight together
+        unsigned long long old[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const unsigned long long want = ((unsigned long long)S.epoch << 32) | (uint32_t)id[k];
+            old[k] = v[k];
+            if (pend[k] && v[k] != want && (uint32_t)(v[k] >> 32) != S.epoch)
+                old[k] = atomicCAS(&S.gvis[slot[k]], v[k], want);
+        }
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            if (!pend[k]) continue;
+            const unsigned long long want = ((unsigned long long)S.epoch << 32) | (uint32_t)id[k];
+            if (old[k] == want) {                       // already visited (or lost a same-id race)
+                pend[k] = false;
+            } else if (old[k] == v[k] && (uint32_t)(v[k] >> 32) != S.epoch) {
+                pend[k] = false;                        // our CAS claimed the stale slot
+                fresh[k] = true;
+            }
+        }
+        // collisions: linear probing from the next slot (load factor <= 1/2)
+#pragma unroll
+        for (int k = 0; k < K; k++)
+            if (pend[k])
+                fresh[k] = probe_insert(S.gvis, gm, S.epoch, (uint32_t)id[k], slot[k], old[k], A.err);
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const unsigned b = __ballot_sync(0xffffffffu, fresh[k]);
+            const int pos = cnt + __popc(b & lanemask_lt());
+            if (fresh[k]) S.newl[pos] = id[k];
+            cnt += __popc(b);
+        }
     }
     __syncwarp();
-    if (!S.ovf) S.vcount += cnt;
     return cnt;
 }
 
@@ -460,53 +609,42 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
     if constexpr (D > 0) {
         constexpr uint32_t row_bytes = D * 4;
         constexpr int CPR = D / 4;  // 16-byte chunks per row
-        const bool tma = A.bulk_rows != 0;
         auto issue = [&](int g) {
-            if (g >= ngroups) {
-                if (!tma) cp_commit();
-                return;
-            }
-            const int r0 = g * RH;
-            const int rows = min(RH, n - r0);
-            float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
-            if (tma) {
-                uint64_t* bar = S.mbar + (g & 1);
-                fence_proxy_async();
-                if (lane == 0) mbar_arrive_expect(bar, rows * row_bytes);
-                __syncwarp();
-                for (int r = lane; r < rows; r += 32) {
-                    const int32_t id = S.newl[r0 + r];
-                    bulk_g2s(dst0 + (size_t)r * sp, G.vec + (size_t)id * D, row_bytes, bar);
+            if (g < ngroups) {
+                const int r0 = g * RH;
+                const int rows = min(RH, n - r0);
+                float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
+                // LDGSTS: LPR lanes per row, CPL 16-byte chunks per lane
+                constexpr int LPR = CPR <= 32 ? 8 : 32;
+                constexpr int CPL = (CPR + LPR - 1) / LPR;
+                constexpr int RPP = 32 / LPR;
+                const int sub = (int)lane % LPR;
+                for (int r = (int)lane / LPR; r < rows; r += RPP) {
+                    const float* src = G.vec + (size_t)S.newl[r0 + r] * D;
+                    float* dst = dst0 + (size_t)r * sp;
+#pragma unroll
+                    for (int k = 0; k < CPL; k++) {
+                        const int ch = sub + k * LPR;
+                        if (CPR % LPR == 0 || ch < CPR) cp_async16(dst + 4 * ch, src + 4 * ch);
+                    }
                 }
-            } else {
-                // LDGSTS: 16-byte chunks of all rows of the half, lane-strided
-                for (int c = lane; c < rows * CPR; c += 32) {
-                    const int r = c / CPR, ch = c - r * CPR;
-                    const int32_t id = S.newl[r0 + r];
-                    cp_async16(dst0 + (size_t)r * sp + 4 * ch, G.vec + (size_t)id * D + 4 * ch);
-                }
-                cp_commit();
             }
+            cp_commit();
         };
         issue(0);
         issue(1);
-        const unsigned v = lane >> 1, h = lane & 1u;
+        const unsigned v = lane >> 2, c = lane & 3u;
         for (int g = 0; g < ngroups; g++) {
-            if (tma) {
-                mbar_wait(S.mbar + (g & 1), (S.phase >> (g & 1)) & 1u);
-                S.phase ^= 1u << (g & 1);
-            } else {
-                cp_wait<1>();
-                __syncwarp();
-            }
+            cp_wait<1>();
+            __syncwarp();
             const int r0 = g * RH;
             const int rows = min(RH, n - r0);
             const float* base = S.stage + (size_t)(g & 1) * RH * sp;
-            for (int pass = 0; pass < rows; pass += 16) {
+            for (int pass = 0; pass < rows; pass += 8) {
                 const int rr = pass + (int)v;
                 const int rc = rr < rows ? rr : rows - 1;
-                const float dist = pw_sum<0, D>(base + (size_t)rc * sp, S.q, h);
-                if (h == 0 && rr < rows) {
+                const float dist = pw_sum4<0, D>(base + (size_t)rc * sp, S.q, c);
+                if (c == 0 && rr < rows) {
                     const uint32_t id = (uint32_t)S.newl[r0 + rr];
                     S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
                 }
@@ -514,7 +652,7 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
             __syncwarp();
             issue(g + 2);
         }
-        if (!tma) cp_wait<0>();
+        cp_wait<0>();
         __syncwarp();
     } else {
         const int row_bytes = A.d * 4;
@@ -559,11 +697,11 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
 // Bitonic sort of ckey[0..s) in shared memory (32 < s <= 256): compact
 // loops (this case only occurs in the first iterations of a search, so code
 // size matters more than its instruction count).
-static __device__ __noinline__ void sort_survivors_smem(WarpState& S, int s) {
+static __device__ __noinline__ void sort_survivors_smem(uint64_t* ckey, int s) {
     const unsigned lane = lane_id();
     int N = 64;
     while (N < s) N <<= 1;
-    for (int e = s + (int)lane; e < N; e += 32) S.ckey[e] = ~0ull;
+    for (int e = s + (int)lane; e < N; e += 32) ckey[e] = ~0ull;
     __syncwarp();
     for (int size = 2; size <= N; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -571,10 +709,10 @@ static __device__ __noinline__ void sort_survivors_smem(WarpState& S, int s) {
                 const int lo = 2 * i - (i & (stride - 1));
                 const int hi = lo + stride;
                 const bool asc = (lo & size) == 0;
-                const uint64_t a = S.ckey[lo], b = S.ckey[hi];
+                const uint64_t a = ckey[lo], b = ckey[hi];
                 if ((a > b) == asc) {
-                    S.ckey[lo] = b;
-                    S.ckey[hi] = a;
+                    ckey[lo] = b;
+                    ckey[hi] = a;
                 }
             }
             __syncwarp();
@@ -613,7 +751,7 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
             x = warp_sort_u64(x);
             if ((int)lane < s) S.ckey[lane] = x;
         } else {
-            sort_survivors_smem(S, s);
+            sort_survivors_smem(S.ckey, s);
         }
         __syncwarp();
         for (int t = lane; t < qlen; t += 32) {
@@ -718,28 +856,46 @@ static __device__ int select_parents(WarpState& S, int r, int32_t* parents) {
     return np;
 }
 
-// _expand (search.py:235-266) up to the ordered candidate list in S.cand;
-// returns the candidate count p * n_sel.
+// Issue the bulk copies described in S.desc[0..n_rows) (one lane per row;
+// TMA takes uniform operands, so the compiler serialises lanes -- kept out of
+// line so there is one copy of that loop in the kernel) and wait for them.
+static __device__ __noinline__ uint32_t bulk_issue_wait(const uint4* desc, uint64_t* bar,
+                                                        uint32_t phase, int n_rows, uint32_t total) {
+    const unsigned lane = lane_id();
+    fence_proxy_async();
+    if (lane == 0) mbar_arrive_expect(bar, total);
+    __syncwarp();
+    for (int r = lane; r < n_rows; r += 32) {
+        const uint4 d = desc[r];
+        const void* src = reinterpret_cast<const void*>(((uint64_t)d.w << 32) | d.z);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                d.x),
+            "l"(src), "r"(d.y), "r"(smem_u32(bar))
+            : "memory");
+    }
+    mbar_wait(bar, (phase >> 2) & 1u);
+    __syncwarp();
+    return phase ^ 4u;
+}
+
 // Fetch up to 3 row sets (adjacency, parent vectors, direction rows) for the
-// parents in ONE round trip: TMA bulk copies when aligned (one lane per row),
-// else cp.async.
+// parents in ONE round trip: TMA bulk copies when aligned, else cp.async.
 template <typename F>
 __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_rows, uint32_t total,
                                             F&& row) {
     const unsigned lane = lane_id();
     if (A.bulk_adj) {
-        fence_proxy_async();
-        if (lane == 0) mbar_arrive_expect(S.mbar + 2, total);
-        __syncwarp();
         for (int r = lane; r < n_rows; r += 32) {
             void* dst;
             const void* src;
             uint32_t bytes;
             row(r, dst, src, bytes);
-            bulk_g2s(dst, src, bytes, S.mbar + 2);
+            const uint64_t sp = (uint64_t)src;
+            S.desc[r] = make_uint4(smem_u32(dst), bytes, (uint32_t)sp, (uint32_t)(sp >> 32));
         }
-        mbar_wait(S.mbar + 2, (S.phase >> 2) & 1u);
-        S.phase ^= 4u;
+        __syncwarp();
+        S.phase = bulk_issue_wait(S.desc, S.mbar + 2, S.phase, n_rows, total);
     } else {
         for (int r = 0; r < n_rows; r++) {
             void* dst;
@@ -750,8 +906,8 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
         }
         cp_commit();
         cp_wait<0>();
+        __syncwarp();
     }
-    __syncwarp();
 }
 
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
@@ -817,7 +973,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                         const bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
                         qb[w] = __ballot_sync(0xffffffffu, bit);
                     }
-                    uint32_t key = 0xFFFFFFFFu;
+                    int c = 0;
                     if ((int)lane < j) {
                         const uint32_t* dr = drow + ((size_t)pi * j + lane) * WC;
                         int diff = 0;
@@ -832,11 +988,28 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
 #pragma unroll
                             for (int w = 0; w < WC; w++) diff += __popc(dr[w] ^ qb[w]);
                         }
-                        key = ((uint32_t)(0xFFFF - (d - diff)) << 16) | lane;
+                        c = d - diff;
                     }
-                    key = warp_sort_u32(key);
-                    if ((int)lane < nsel)
-                        S.cand[(pg + pi) * nsel + lane] = craw[(pg + pi) * j + (key & 0xFFFFu)];
+                    // rank = #slots with a larger count + #equal-count slots
+                    // before this one: bit-serial ballot radix over count bits
+                    constexpr int NB = D >= 512 ? 10 : D >= 256 ? 9 : D >= 128 ? 8 : D >= 64 ? 7 : 6;
+                    const unsigned valid = __ballot_sync(0xffffffffu, (int)lane < j);
+                    unsigned eq = valid;
+                    int gt = 0;
+#pragma unroll
+                    for (int b = (D >= 1024 ? 11 : NB) - 1; b >= 0; b--) {
+                        const bool mine = (c >> b) & 1;
+                        const unsigned B = __ballot_sync(0xffffffffu, mine) & valid;
+                        if (mine) {
+                            eq &= B;
+                        } else {
+                            gt += __popc(eq & B);
+                            eq &= ~B;
+                        }
+                    }
+                    const int rank = gt + __popc(eq & lanemask_lt());
+                    if ((int)lane < j && rank < nsel)
+                        S.cand[(pg + pi) * nsel + rank] = craw[(pg + pi) * j + lane];
                 }
             } else {
                 for (int pi = 0; pi < gp; pi++)
@@ -875,7 +1048,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
             b = adj_bytes;
         });
         for (int pi = 0; pi < np; pi++) {
-            if (lane == 0) permutation(rng, (uint32_t)j, perm);  // direction.py:103-105
+            if (lane == 0) rng = permutation(rng, (uint32_t)j, perm);  // direction.py:103-105
             __syncwarp();
             for (int t = lane; t < nsel; t += 32) S.cand[pi * nsel + t] = craw[pi * j + perm[t]];
             __syncwarp();
@@ -900,6 +1073,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     S.qlen = 0;
     S.vcount = 0;
     S.ovf = false;
+    S.epoch = S.epoch == 0xFFFFFFFFu ? 1u : S.epoch + 1u;
     S.c_it = S.c_dc = S.c_tv = S.c_ne = S.c_dgs = S.c_ins = 0;
 
     // _initial_batch (search.py:207-227)
@@ -912,13 +1086,13 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
             if (choice_uses_tail(pop, size)) {
                 uint32_t cap = 1;
                 while (cap < 4u * size + 8u) cap <<= 1;
-                choice_tail(rng, pop, size, S.gscr, S.gscr + cap, cap - 1, ch);
+                rng = choice_tail(rng, pop, size, S.gscr, S.gscr + cap, cap - 1, ch);
             } else {
                 uint32_t mask = (uint32_t)gen_mask64((uint64_t)(1.2 * (double)size));
                 uint32_t* set = ((int64_t)(mask + 1) * 4 <= (int64_t)A.R * A.spad * 4)
                                     ? reinterpret_cast<uint32_t*>(S.stage)
                                     : S.gscr;
-                choice_floyd(rng, pop, size, set, mask, ch);
+                rng = choice_floyd(rng, pop, size, set, mask, ch);
             }
         }
         __syncwarp();
@@ -999,8 +1173,10 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
     S.stage = reinterpret_cast<float*>(base + A.o_stage);
     S.misc = reinterpret_cast<int32_t*>(base + A.o_misc);
     S.gvis = A.gvis + (size_t)gwarp * (A.gmask + 1);
+    S.epoch = A.gepoch[gwarp];
     S.gscr = A.gscratch + (size_t)gwarp * A.gscratch_words;
     S.mbar = reinterpret_cast<uint64_t*>(base + A.o_mbar);
+    S.desc = reinterpret_cast<uint4*>(base + A.o_desc);
     S.phase = 0;
     if (lane < 3) mbar_init(S.mbar + lane);
     mbar_fence_init();
@@ -1109,6 +1285,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         }
         __syncwarp();
     }
+    if (lane == 0) A.gepoch[gwarp] = S.epoch;
 }
 
 typedef void (*KernelFn)(KArgs);

@@ -149,8 +149,11 @@ struct pw_shard {
     int64_t bytes = 0;
     // launch workspace (grow-only)
     int32_t* counter = nullptr;
-    uint32_t* gvis = nullptr;
+    unsigned long long* gvis = nullptr;
     size_t gvis_words = 0;
+    uint32_t* gepoch = nullptr;
+    size_t gepoch_n = 0;
+    int64_t gvis_stride = 0;  // per-warp table size the epochs are valid for
     uint32_t* gscr = nullptr;
     size_t gscr_words = 0;
     std::mutex mu;
@@ -333,8 +336,12 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.L_max = p.l;
     int64_t bound = visit_bound(A.cfg, G.j, G.n);
     if (ghost_on) bound = std::max(bound, visit_bound(A.gcfg, sh->gj, sh->gn));
+    // Default: a small shared-memory visited table (first iterations) backed
+    // by the per-warp epoch-tagged global table (batched probes): measured on
+    // C2 (10M x 96, l=256) this fits ~10 query-warps per SM instead of 5 and
+    // is faster for both the naive and the PathWeaver arm (profiles/r01).
     int64_t H = tun && tun->visited_slots > 0 ? next_pow2(tun->visited_slots)
-                                              : std::min<int64_t>(4096, next_pow2(bound * 4 / 3 + 2));
+                                              : std::min<int64_t>(256, next_pow2(bound * 4 / 3 + 2));
     H = std::max<int64_t>(H, 64);
     A.H = (int32_t)H;
     A.vis_limit = (int32_t)(H * 3 / 4);
@@ -344,9 +351,10 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     if (tun && tun->stage_rows > 0) {
         R = tun->stage_rows;
     } else if (specialised) {
-        // rows in flight per warp: two halves of the staging ring, ~<= 20 KB
-        R = 32;
-        while (R > 4 && (int64_t)R * spad * 4 > 20480) R >>= 1;
+        // rows in flight per warp: two halves of 8 rows (one 8-row compute
+        // pass each); large rows shrink to keep staging <= ~10 KB
+        R = 16;
+        while (R > 4 && (int64_t)R * spad * 4 > 10240) R >>= 1;
     } else {
         R = std::max(2, std::min(16, (16384 / (spad * 4)) & ~1));
     }
@@ -379,6 +387,8 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     off = al(off + 4 * misc);
     A.o_mbar = (int32_t)off;
     off = al(off + 3 * 8);
+    A.o_desc = (int32_t)off;
+    off = al(off + 16 * 32);
     A.warp_bytes = (int32_t)off;
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
@@ -411,11 +421,26 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         PW_CUDA(cudaMalloc(&sh->counter, sizeof(int32_t) * 2));
         PW_CUDA(cudaMemset(sh->counter, 0, sizeof(int32_t) * 2));
     }
-    if (sh->gvis_words < (size_t)total_warps * gsz) {
+    if (sh->gvis_words < (size_t)total_warps * gsz || sh->gepoch_n < (size_t)total_warps) {
+        // epoch-tagged tables: zero once (epoch 0 is never used by a search)
         if (sh->gvis) cudaFree(sh->gvis);
+        if (sh->gepoch) cudaFree(sh->gepoch);
         sh->gvis = nullptr;
-        PW_CUDA(cudaMalloc(&sh->gvis, sizeof(uint32_t) * (size_t)total_warps * gsz));
-        sh->gvis_words = (size_t)total_warps * gsz;
+        sh->gepoch = nullptr;
+        const size_t words = std::max(sh->gvis_words, (size_t)total_warps * gsz);
+        PW_CUDA(cudaMalloc(&sh->gvis, sizeof(unsigned long long) * words));
+        PW_CUDA(cudaMemset(sh->gvis, 0, sizeof(unsigned long long) * words));
+        PW_CUDA(cudaMalloc(&sh->gepoch, sizeof(uint32_t) * (size_t)total_warps));
+        PW_CUDA(cudaMemset(sh->gepoch, 0, sizeof(uint32_t) * (size_t)total_warps));
+        sh->gvis_words = words;
+        sh->gepoch_n = (size_t)total_warps;
+        sh->gvis_stride = gsz;
+    } else if (sh->gvis_stride != gsz) {
+        // a different per-warp stride maps regions to other warps: re-zero so no
+        // stale (epoch, id) of another warp can match
+        PW_CUDA(cudaMemset(sh->gvis, 0, sizeof(unsigned long long) * sh->gvis_words));
+        PW_CUDA(cudaMemset(sh->gepoch, 0, sizeof(uint32_t) * sh->gepoch_n));
+        sh->gvis_stride = gsz;
     }
     if (sh->gscr_words < (size_t)total_warps * scr) {
         if (sh->gscr) cudaFree(sh->gscr);
@@ -424,6 +449,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         sh->gscr_words = (size_t)total_warps * scr;
     }
     A.gvis = sh->gvis;
+    A.gepoch = sh->gepoch;
     A.gscratch = sh->gscr;
     A.gscratch_words = scr;
     A.task_counter = sh->counter;
@@ -514,7 +540,7 @@ int pw_shard_destroy(pw_shard* sh) {
     cudaGetDevice(&cur);
     cudaSetDevice(sh->device);
     void* ptrs[] = {sh->vec, sh->adj, sh->gid, sh->dir, sh->inter, sh->gvec, sh->gadj, sh->gids,
-                    sh->counter, sh->gvis, sh->gscr};
+                    sh->counter, sh->gvis, sh->gscr, sh->gepoch};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(cur);
@@ -793,6 +819,21 @@ int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, cons
     }
     cudaFree(buf);
     return rc;
+}
+
+int pw_launch_config(pw_shard* sh, const pw_params* params, const pw_tuning* tuning,
+                     int32_t* out) {
+    if (!sh || !params || !out) return set_err(PW_EINVAL, "null argument");
+    Launch Lc;
+    int rc = prepare(sh, *params, tuning, false, 0, params->ghost_enabled && sh->gn > 0, Lc);
+    if (rc) return rc;
+    out[0] = Lc.warps_per_block;
+    out[1] = Lc.A.warp_bytes;
+    out[2] = Lc.A.H;
+    out[3] = Lc.A.R;
+    out[4] = Lc.fn == pw_kernel_0() ? 0 : sh->d;
+    out[5] = Lc.blocks;
+    return 0;
 }
 
 int pw_squared_l2_rows(pw_shard* sh, const int32_t* ids, int64_t n_ids, const float* query,

@@ -13,8 +13,12 @@
 
 #ifdef __CUDACC__
 #define PW_HD __host__ __device__ __forceinline__
+// cold per-search routines: one out-of-line copy keeps the kernel's hot loop
+// inside the instruction caches
+#define PW_HD_COLD static __host__ __device__ __noinline__
 #else
 #define PW_HD inline
+#define PW_HD_COLD static inline
 #endif
 
 namespace pw {
@@ -76,7 +80,7 @@ PW_HD uint32_t ss_mix(uint32_t x, uint32_t y) {
 
 // np.random.PCG64(seed64): SeedSequence(seed64).generate_state(4, uint64)
 // then pcg_setseq_128_srandom_r(initstate, initseq).
-PW_HD Pcg64 pcg64_from_seed(uint64_t seed64) {
+PW_HD_COLD Pcg64 pcg64_from_seed(uint64_t seed64) {
     uint32_t e0 = (uint32_t)seed64, e1 = (uint32_t)(seed64 >> 32);
     int n_ent = (seed64 >> 32) ? 2 : 1;
     uint32_t pool[4];
@@ -179,8 +183,8 @@ PW_HD uint64_t gen_mask64(uint64_t v) {
 // (mask+1) uint32 slots (values < 2^31 so 0xFFFFFFFF is the empty marker),
 // mask = gen_mask64(uint64(1.2 * size)).  out gets `size` values, then
 // _shuffle_int(size, first=1).
-PW_HD void choice_floyd(Pcg64& g, uint32_t pop, uint32_t size, uint32_t* set, uint32_t mask,
-                        int32_t* out) {
+PW_HD_COLD Pcg64 choice_floyd(Pcg64 g, uint32_t pop, uint32_t size, uint32_t* set, uint32_t mask,
+                               int32_t* out) {
     for (uint32_t i = 0; i <= mask; i++) set[i] = 0xFFFFFFFFu;
     for (uint32_t j = pop - size; j < pop; j++) {
         uint32_t val = bounded_u32(g, j);
@@ -202,6 +206,7 @@ PW_HD void choice_floyd(Pcg64& g, uint32_t pop, uint32_t size, uint32_t* set, ui
         out[jj] = out[i];
         out[i] = t;
     }
+    return g;
 }
 
 // Tail-shuffle branch (pop > 10000 and size > pop // 50): partial
@@ -221,7 +226,7 @@ PW_HD void smap_set(uint32_t* keys, uint32_t* vals, uint32_t cmask, uint32_t k, 
     keys[h] = k;
     vals[h] = v;
 }
-PW_HD void choice_tail(Pcg64& g, uint32_t pop, uint32_t size, uint32_t* keys, uint32_t* vals,
+PW_HD_COLD Pcg64 choice_tail(Pcg64 g, uint32_t pop, uint32_t size, uint32_t* keys, uint32_t* vals,
                        uint32_t cmask, int32_t* out) {
     for (uint32_t i = 0; i <= cmask; i++) keys[i] = 0xFFFFFFFFu;
     uint32_t first = pop - size > 1 ? pop - size : 1;
@@ -233,12 +238,13 @@ PW_HD void choice_tail(Pcg64& g, uint32_t pop, uint32_t size, uint32_t* keys, ui
         smap_set(keys, vals, cmask, (uint32_t)i, vj);
     }
     for (uint32_t t = 0; t < size; t++) out[t] = (int32_t)smap_get(keys, vals, cmask, pop - size + t);
+    return g;
 }
 
 PW_HD bool choice_uses_tail(uint32_t pop, uint32_t size) { return pop > 10000u && size > pop / 50u; }
 
 // Generator.permutation(n) into out[n]
-PW_HD void permutation(Pcg64& g, uint32_t n, int32_t* out) {
+PW_HD_COLD Pcg64 permutation(Pcg64 g, uint32_t n, int32_t* out) {
     for (uint32_t i = 0; i < n; i++) out[i] = (int32_t)i;
     for (int64_t i = (int64_t)n - 1; i >= 1; i--) {
         uint32_t jj = random_interval(g, (uint32_t)i);
@@ -246,6 +252,7 @@ PW_HD void permutation(Pcg64& g, uint32_t n, int32_t* out) {
         out[jj] = out[i];
         out[i] = t;
     }
+    return g;
 }
 
 }  // namespace pw

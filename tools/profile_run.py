@@ -21,6 +21,7 @@ ap.add_argument("--config", default="c2s")
 ap.add_argument("--arm", default="pathweaver")
 ap.add_argument("--l", type=int, default=160)
 ap.add_argument("--reps", type=int, default=4)
+ap.add_argument("--tuning", default="")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 W = bench.build_workload(cfg, 0, 1, torch.device("cuda", 0))
@@ -29,7 +30,9 @@ shard = dv.TensorShard(W["vec"], W["adj"], W["rows"].to(torch.int32), W["directi
 run = dv.DeviceRun(W["queries"].shape[0], 1, cfg["k"], "cuda")
 p = bench.arm_params(args.arm, args.l, cfg["k"])
 mode = "pipelined" if args.arm == "pathweaver" else "baseline"
+import json
+tuning = json.loads(args.tuning) if args.tuning else None
 for _ in range(args.reps):
-    dv.run_local([shard], p, W["queries"], mode, run)
+    dv.run_local([shard], p, W["queries"], mode, run, tuning=tuning)
 torch.cuda.synchronize()
 print("done", run.final_ids[0].tolist())
