@@ -107,6 +107,10 @@ def lib():
                               C.POINTER(_Params), C.c_int32, C.c_int32] + [C.c_void_p] * 7
         L.orc_reduce_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                       C.c_void_p, C.c_void_p]
+        L.orc_run_stage.argtypes = [C.POINTER(_Shard), C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                    C.POINTER(_Params), C.c_int32, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                    C.c_void_p, C.c_int32]
         _LIB = L
     return _LIB
 
@@ -316,3 +320,19 @@ def reduce_topk(ids, dists, k: int):
     if rc < 0:
         raise ValueError(_err())
     return oi[:rc], od[:rc]
+
+
+def run_stage(ctx, queries: np.ndarray, q0: int, n: int, params, stage: int, entries_in, forward_out,
+              shard_ids, shard_dists, col: int, stats_i32, stats_i64, threads: int = 0) -> None:
+    """One stage of one shard on the CPU (mirror of pw_search_stage); the
+    output arrays are numpy arrays updated in place."""
+    keep = _Keep()
+    sh = _shard(keep, ctx)
+    q = keep.arr(queries, np.float32)
+    p = _params(params)
+    rc = lib().orc_run_stage(C.byref(sh), q.ctypes.data, q.shape[0], q0, n, C.byref(p), stage,
+                             _ptr(entries_in), _ptr(forward_out), shard_ids.ctypes.data,
+                             shard_dists.ctypes.data, shard_ids.shape[1], col,
+                             stats_i32.ctypes.data, stats_i64.ctypes.data, int(threads))
+    if rc:
+        raise ValueError(_err())

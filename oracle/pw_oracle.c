@@ -695,6 +695,40 @@ static int search_one(run_t* R, int64_t qid, int32_t shard, int32_t stage, int h
     return rc;
 }
 
+int orc_run_stage(const orc_shard* shard, const float* queries, int64_t q_total, int64_t q0,
+                  int64_t n, const orc_params* p, int32_t stage, const int32_t* entries_in,
+                  int32_t* forward_out, int32_t* shard_ids, float* shard_dists, int32_t n_cols,
+                  int32_t col, int32_t* stats_i32, int64_t* stats_i64, int32_t threads) {
+    /* the per-query dispatcher indexes shards[shard]; present this one shard at
+     * index `col` of a virtual array so search_one's output column is col */
+    orc_shard* arr = (orc_shard*)calloc((size_t)n_cols, sizeof(orc_shard));
+    arr[col] = *shard;
+    /* search_one writes stats at [stage*4*Q]: point the bases so stage maps to row 0 */
+    run_t R = {arr, n_cols, queries, q_total, shard->main.d, p, shard_ids, shard_dists,
+               stats_i32 - (int64_t)stage * 4 * q_total, stats_i64 - (int64_t)stage * 4 * q_total};
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#else
+    (void)threads;
+#endif
+    volatile int err = 0;
+    char errbuf[256] = {0};
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int64_t qi = q0; qi < q0 + n; qi++) {
+        if (err) continue;
+        int32_t tl = -1;
+        if (search_one(&R, qi, col, stage, entries_in != NULL, entries_in ? entries_in[qi] : 0, &tl)) {
+#pragma omp critical
+            { err = 1; snprintf(errbuf, sizeof errbuf, "%s", g_err); }
+            continue;
+        }
+        if (forward_out) forward_out[qi] = shard->inter_map[tl];
+    }
+    free(arr);
+    if (err) { snprintf(g_err, sizeof g_err, "%s", errbuf); return -1; }
+    return 0;
+}
+
 int orc_run(const orc_shard* shards, int32_t n_shards, const float* queries, int64_t q,
             const orc_params* p, int32_t mode, int32_t threads,
             int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,

@@ -114,6 +114,16 @@ int orc_run(const orc_shard* shards, int32_t n_shards, const float* queries, int
             int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
             int32_t* stats_i32, int64_t* stats_i64, int64_t* comm);
 
+/* One stage launch, mirroring pw_search_stage: queries [q0, q0+n) of the
+ * (q_total, d) array searched on one shard at `stage` (pipeline.py:329-342 /
+ * :294-297).  entries_in/forward_out: (q_total,) or NULL; shard_ids/dists:
+ * (q_total, n_cols, k) written at column col; stats_i32 (4, q_total) /
+ * stats_i64 (4, q_total) accumulate as in orc_run. */
+int orc_run_stage(const orc_shard* shard, const float* queries, int64_t q_total, int64_t q0,
+                  int64_t n, const orc_params* p, int32_t stage, const int32_t* entries_in,
+                  int32_t* forward_out, int32_t* shard_ids, float* shard_dists, int32_t n_cols,
+                  int32_t col, int32_t* stats_i32, int64_t* stats_i64, int32_t threads);
+
 /* pipeline.py:187-196 reduce_topk over one query's n candidates. returns count or -1. */
 int orc_reduce_topk(const int32_t* ids, const float* dists, int64_t n, int32_t k,
                     int32_t* out_ids, float* out_dists);

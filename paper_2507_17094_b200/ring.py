@@ -45,22 +45,21 @@ def comm_stage_bytes(q: int, world: int) -> np.ndarray:
     return out
 
 
-def run_ring_pipelined(stage_fn, q: int, rank: int, world: int, send_recv, on_stage_done=None):
-    """Drive the pipelined ring for this rank.
+def run_ring_pipelined(stage_fn, q: int, rank: int, world: int, send_recv) -> None:
+    """Drive this rank through the pipelined ring (pipeline.py:327-347).
 
-    stage_fn(stage, q0, n, entries_or_None) -> forward entries (n,) int32 or None
-    send_recv(send_array, recv_count) -> received array (exchange with g+1 / g-1)
+    stage_fn(stage, q0, n, has_entries) searches chunk [q0, q0+n) on this
+    rank's shard and returns its forward payload (inter_map[top1] per query);
+    send_recv(payload, next_q0, next_n) sends the payload to rank+1 and
+    receives, from rank-1, the entries of the chunk this rank searches next.
     """
     lo = chunk_bounds(q, world)
-    entries = None
     for stage in range(world):
         c = ring_schedule(rank, world, stage)
-        fwd = stage_fn(stage, lo[c], lo[c + 1] - lo[c], entries)
+        fwd = stage_fn(stage, lo[c], lo[c + 1] - lo[c], stage > 0)
         if stage < world - 1:
-            c_next = ring_schedule(rank, world, stage + 1)
-            entries = send_recv(fwd, lo[c_next + 1] - lo[c_next])
-        if on_stage_done is not None:
-            on_stage_done(stage)
+            cn = ring_schedule(rank, world, stage + 1)
+            send_recv(fwd, lo[cn], lo[cn + 1] - lo[cn])
 
 
 class RingSearch:
@@ -111,19 +110,20 @@ class RingSearch:
             launch(g, 0, self.q, None, None)
         else:
             ein, eout = R.entries
-            lo = chunk_bounds(self.q, N)
-            for stage in range(N):
-                c = ring_schedule(g, N, stage)
-                launch(stage, lo[c], lo[c + 1] - lo[c], ein if stage > 0 else None,
-                       eout if stage < N - 1 else None)
-                if stage < N - 1:
-                    cn = ring_schedule(g, N, stage + 1)
-                    send = eout[lo[c]:lo[c + 1]]
-                    recv = ein[lo[cn]:lo[cn + 1]]
-                    ops = [dist.P2POp(dist.isend, send, (g + 1) % N),
-                           dist.P2POp(dist.irecv, recv, (g - 1) % N)]
-                    for w in dist.batch_isend_irecv(ops):
-                        w.wait()
+
+            def stage_fn(stage, q0, n, has_entries):
+                launch(stage, q0, n, ein if has_entries else None, eout if stage < N - 1 else None)
+                return eout[q0:q0 + n]
+
+            def send_recv(payload, next_q0, next_n):
+                # 4 B per query over NVLink (pipeline.py:339-341): NCCL P2P on the
+                # compute stream's order, so stage s+1 starts when its entries land
+                ops = [dist.P2POp(dist.isend, payload, (g + 1) % N),
+                       dist.P2POp(dist.irecv, ein[next_q0:next_q0 + next_n], (g - 1) % N)]
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+
+            run_ring_pipelined(stage_fn, self.q, g, N, send_recv)
         # all-gather this rank's column of the candidate lists, then reduce (K2)
         col_ids = R.shard_ids[:, g, :].contiguous()
         col_d = R.shard_dists[:, g, :].contiguous()
