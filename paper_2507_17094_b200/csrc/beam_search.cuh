@@ -524,11 +524,15 @@ static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint3
 // the (now read-only) shared table is resolved against the per-warp global
 // epoch table with all of a lane's probes in flight at once: first-slot
 // loads, then CASes, then (rarely) linear-probing retries.
-static __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
+// GLOBAL_ONLY (the specialised kernels): the shared table is skipped and every
+// probe goes to the per-warp epoch table, so only the batched-probe path below
+// is compiled into the hot loop.
+template <bool GLOBAL_ONLY>
+__device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
     const unsigned lane = lane_id();
-    if (!S.ovf && S.vcount + nb > A.vis_limit) S.ovf = true;
+    if (!GLOBAL_ONLY && !S.ovf && S.vcount + nb > A.vis_limit) S.ovf = true;
     int cnt = 0;
-    if (!S.ovf) {
+    if (!GLOBAL_ONLY && !S.ovf) {
         for (int base = 0; base < nb; base += 32) {
             int t = base + lane;
             int32_t id = t < nb ? S.newl[t] : -1;
@@ -553,7 +557,7 @@ static __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
         for (int k = 0; k < K; k++) {
             const int t = base0 + k * 32 + (int)lane;
             id[k] = t < nb ? S.newl[t] : -1;
-            pend[k] = t < nb && !smem_lookup(A, S, (uint32_t)id[k]);
+            pend[k] = t < nb && (GLOBAL_ONLY || !smem_lookup(A, S, (uint32_t)id[k]));
             slot[k] = (hash32((uint32_t)id[k] ^ 0x5bd1e995u) >> 3) & gm;
             v[k] = pend[k] ? S.gvis[slot[k]] : 0ull;
             fresh[k] = false;
@@ -879,35 +883,50 @@ static __device__ __noinline__ uint32_t bulk_issue_wait(const uint4* desc, uint6
     return phase ^ 4u;
 }
 
+// cp.async fallback for rows that are not 16-byte multiples (out of line).
+static __device__ __noinline__ void copy_issue_wait(const uint4* desc, int n_rows) {
+    const unsigned lane = lane_id();
+    for (int r = 0; r < n_rows; r++) {
+        const uint4 d = desc[r];
+        const char* src = reinterpret_cast<const char*>(((uint64_t)d.w << 32) | d.z);
+        const uint32_t dst = d.x, bytes = d.y;
+        const uint32_t al = (uint32_t)(uintptr_t)src | dst | bytes;
+        if ((al & 15u) == 0) {
+            for (uint32_t c = lane; c < (bytes >> 4); c += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * c), "l"(src + 16 * c));
+        } else if ((al & 7u) == 0) {
+            for (uint32_t c = lane; c < (bytes >> 3); c += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst + 8 * c), "l"(src + 8 * c));
+        } else {
+            for (uint32_t c = lane; c < (bytes >> 2); c += 32)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst + 4 * c), "l"(src + 4 * c));
+        }
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+}
+
 // Fetch up to 3 row sets (adjacency, parent vectors, direction rows) for the
-// parents in ONE round trip: TMA bulk copies when aligned, else cp.async.
+// parents in ONE round trip: lanes write one descriptor per row, then a single
+// out-of-line issuer runs TMA bulk copies (aligned rows) or cp.async.
 template <typename F>
 __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_rows, uint32_t total,
                                             F&& row) {
     const unsigned lane = lane_id();
-    if (A.bulk_adj) {
-        for (int r = lane; r < n_rows; r += 32) {
-            void* dst;
-            const void* src;
-            uint32_t bytes;
-            row(r, dst, src, bytes);
-            const uint64_t sp = (uint64_t)src;
-            S.desc[r] = make_uint4(smem_u32(dst), bytes, (uint32_t)sp, (uint32_t)(sp >> 32));
-        }
-        __syncwarp();
-        S.phase = bulk_issue_wait(S.desc, S.mbar + 2, S.phase, n_rows, total);
-    } else {
-        for (int r = 0; r < n_rows; r++) {
-            void* dst;
-            const void* src;
-            uint32_t bytes;
-            row(r, dst, src, bytes);
-            warp_copy_async(dst, src, (int)bytes);
-        }
-        cp_commit();
-        cp_wait<0>();
-        __syncwarp();
+    for (int r = lane; r < n_rows; r += 32) {
+        void* dst;
+        const void* src;
+        uint32_t bytes;
+        row(r, dst, src, bytes);
+        const uint64_t sp = (uint64_t)src;
+        S.desc[r] = make_uint4(smem_u32(dst), bytes, (uint32_t)sp, (uint32_t)(sp >> 32));
     }
+    __syncwarp();
+    if (A.bulk_adj)
+        S.phase = bulk_issue_wait(S.desc, S.mbar + 2, S.phase, n_rows, total);
+    else
+        copy_issue_wait(S.desc, n_rows);
 }
 
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
@@ -1067,7 +1086,8 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
                            int64_t* n_logged) {
     const unsigned lane = lane_id();
     // reset per-search state
-    for (int i = lane; i < A.H; i += 32) S.vh[i] = kEmpty;
+    if (D == 0)
+        for (int i = lane; i < A.H; i += 32) S.vh[i] = kEmpty;
     bh_clear(A, S);
     S.cur = 0;
     S.qlen = 0;
@@ -1110,7 +1130,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         nb = cnt;
     }
     bh_clear(A, S);
-    int n_new = visited_filter(A, S, nb);
+    int n_new = visited_filter<(D > 0)>(A, S, nb);
 
     bool converged = false;
     int32_t* parents = S.misc + A.PG * G.j + A.PG * A.W + 8;
@@ -1145,7 +1165,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
         S.c_tv += nb;
         bh_clear(A, S);
-        n_new = visited_filter(A, S, nb);
+        n_new = visited_filter<(D > 0)>(A, S, nb);
     }
     return converged;
 }

@@ -340,13 +340,18 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // by the per-warp epoch-tagged global table (batched probes): measured on
     // C2 (10M x 96, l=256) this fits ~10 query-warps per SM instead of 5 and
     // is faster for both the naive and the PathWeaver arm (profiles/r01).
-    int64_t H = tun && tun->visited_slots > 0 ? next_pow2(tun->visited_slots)
-                                              : std::min<int64_t>(256, next_pow2(bound * 4 / 3 + 2));
-    H = std::max<int64_t>(H, 64);
-    A.H = (int32_t)H;
-    A.vis_limit = (int32_t)(H * 3 / 4);
     Lc.fn = pick_kernel(d);
     const bool specialised = Lc.fn != pw_kernel_0();
+    // Specialised kernels keep the exact visited set only in the per-warp
+    // epoch-tagged global table (batched probes; no shared table, which buys
+    // resident warps).  The generic-d kernel uses a shared table spilling to
+    // the same global table.
+    int64_t H = specialised ? 0
+                            : (tun && tun->visited_slots > 0 ? next_pow2(tun->visited_slots)
+                                                             : std::min<int64_t>(256, next_pow2(bound * 4 / 3 + 2)));
+    if (!specialised) H = std::max<int64_t>(H, 64);
+    A.H = (int32_t)H;
+    A.vis_limit = (int32_t)(H * 3 / 4);
     int R;
     if (tun && tun->stage_rows > 0) {
         R = tun->stage_rows;
@@ -412,7 +417,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     const int total_warps = Lc.blocks * wpb;
     // the spill triggers when (smem entries + batch) > vis_limit, so a table is
     // needed whenever bound + CB can exceed it; it holds <= bound entries
-    int64_t gsz = bound + cb > A.vis_limit ? next_pow2(2 * bound + 2) : 1;
+    int64_t gsz = (specialised || bound + cb > A.vis_limit) ? next_pow2(2 * bound + 2) : 1;
     A.gmask = (int32_t)(gsz - 1);
     int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
     int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
