@@ -326,7 +326,7 @@ def run_ours(args, cfg):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": None,
+                         "traffic": traffic_for(cfg, ops["pathweaver"]["l"]),
                          "kernel": "beam_search_kernel",
                          "algorithmic_bytes_per_step": int(bytes_step),
                          "kernel_ms_per_step": round(kern_ms / args.steps, 4),
@@ -345,6 +345,19 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def traffic_for(cfg: dict, l: int):
+    """DRAM bytes (read + write) per K1 launch from the latest committed ncu
+    --set full capture of the same workload/operating point, else None."""
+    for path in sorted((ROOT / "profiles").glob("r*/k1_traffic.json"), reverse=True):
+        try:
+            t = json.loads(path.read_text())
+        except (OSError, ValueError):
+            continue
+        if t.get("workload") == cfg["workload"] and t.get("l") == l:
+            return int(t["traffic_bytes_per_launch"])
+    return None
 
 
 def host_index(W: dict):
