@@ -56,7 +56,8 @@ typedef struct {
     int32_t visited_slots;   /* shared-memory visited-hash slots per query (power of 2) */
     int32_t stage_rows;      /* rows in flight per warp (gather staging) */
     int32_t warps_per_sm;    /* cap on resident query-warps per SM */
-    int32_t row_copy;        /* vector-row gathers: 0 cp.async (LDGSTS), 1 TMA cp.async.bulk */
+    int32_t row_copy;        /* reserved (vector rows always use cp.async; TMA measured slower) */
+    int32_t flags;           /* bit 0: L2-prefetch predicted parent rows (off by default: measured slower) */
 } pw_tuning;
 
 /* One shard (pipeline.py:121-155 build_contexts output for one ShardPack):

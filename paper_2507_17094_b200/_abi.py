@@ -31,7 +31,7 @@ class Params(C.Structure):
 
 class Tuning(C.Structure):
     _fields_ = [("visited_slots", C.c_int32), ("stage_rows", C.c_int32),
-                ("warps_per_sm", C.c_int32), ("row_copy", C.c_int32)]
+                ("warps_per_sm", C.c_int32), ("row_copy", C.c_int32), ("flags", C.c_int32)]
 
 
 class ShardDesc(C.Structure):
@@ -132,9 +132,9 @@ def params_struct(p) -> Params:
 
 def tuning_struct(t) -> Tuning:
     if t is None:
-        return Tuning(0, 0, 0, 0)
+        return Tuning(0, 0, 0, 0, 0)
     return Tuning(int(t.get("visited_slots", 0)), int(t.get("stage_rows", 0)),
-                  int(t.get("warps_per_sm", 0)), int(t.get("row_copy", 0)))
+                  int(t.get("warps_per_sm", 0)), int(t.get("row_copy", 0)), int(t.get("flags", 0)))
 
 
 def launch_config(shard_handle, params, tuning=None) -> dict:

@@ -97,6 +97,7 @@ struct KArgs {
         o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
     int32_t bulk_adj;       // adjacency / direction rows may use cp.async.bulk
+    int32_t prefetch;       // L2-prefetch predicted parent rows
     int32_t vis_limit;      // smem visited entries before spilling to global
     unsigned long long* gvis;  // per-warp global visited spill tables, (epoch << 32 | id)
     int32_t gmask;
@@ -173,10 +174,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // ---- warp-wide bitonic sorts (ascending across lanes)
 __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
+    // rolled network (15 compare-exchange stages): compact code for the
+    // instruction caches; the stage parameters are uniform
     const unsigned lane = threadIdx.x & 31u;
-#pragma unroll
+#pragma unroll 1
     for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
+#pragma unroll 1
         for (int j = k >> 1; j > 0; j >>= 1) {
             uint64_t o = __shfl_xor_sync(0xffffffffu, x, j);
             bool keep_min = ((lane & j) == 0) == ((lane & k) == 0);
@@ -546,7 +549,7 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
         S.vcount += cnt;
         return cnt;
     }
-    constexpr int K = 8;
+    constexpr int K = 4;
     const uint32_t gm = (uint32_t)A.gmask;
     for (int base0 = 0; base0 < nb; base0 += 32 * K) {
         int32_t id[K];
@@ -929,6 +932,38 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
         copy_issue_wait(S.desc, n_rows);
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Warm L2 with the rows the next expansion will most likely fetch: the first
+// r unexpanded entries of the current queue become the parents unless new
+// candidates overtake them.  One prefetch per 128-byte line, no registers
+// tied up; a wrong guess only costs bandwidth.
+template <int D>
+__device__ __forceinline__ void prefetch_parents(const KArgs& A, const WarpState& S, const GraphDev& G,
+                                                 const SearchCfg& C) {
+    const unsigned lane = lane_id();
+    const uint64_t* qk = S.qk_cur();
+    const uint8_t* qe = S.qe_cur();
+    const int lim = min(S.qlen, 32);
+    const bool f = (int)lane < lim && qe[lane] == 0;
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    const int rank = __popc(b & lanemask_lt());
+    if (!f || rank >= C.r) return;
+    const uint32_t par = (uint32_t)qk[lane];
+    const int j = G.j;
+    const char* a = reinterpret_cast<const char*>(G.adj + (size_t)par * j);
+    for (int o = 0; o < j * 4; o += 128) prefetch_l2(a + o);
+    if (C.prune_sel == 1 && G.dir) {
+        const int d = D > 0 ? D : A.d;
+        const char* v = reinterpret_cast<const char*>(G.vec + (size_t)par * d);
+        for (int o = 0; o < d * 4; o += 128) prefetch_l2(v + o);
+        const char* dr = reinterpret_cast<const char*>(G.dir + (size_t)par * j * A.W);
+        for (int o = 0; o < j * A.W * 4; o += 128) prefetch_l2(dr + o);
+    }
+}
+
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
 // returns the candidate count p * n_sel.
 template <int D>
@@ -1137,6 +1172,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     for (int it = 0; it < C.max_iter; it++) {
         S.c_it++;
         int inserted = 0;
+        if (A.prefetch && it > 0 && it < C.max_iter - 1) prefetch_parents<D>(A, S, G, C);
         if (n_new) {
             if (C.log && A.visit_log) {
                 for (int t = lane; t < n_new; t += 32) {

@@ -397,7 +397,8 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.warp_bytes = (int32_t)off;
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
-    A.bulk_rows = (specialised && tun && tun->row_copy == 1) ? 1 : 0;
+    A.bulk_rows = 0;
+    A.prefetch = (tun && (tun->flags & 1)) ? 1 : 0;
     A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
                   (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16(4ll * d) && b16(4ll * G.j * W))))
                      ? 1
