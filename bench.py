@@ -174,11 +174,18 @@ def run_ours(args, cfg):
 
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # NCCL over NVLink in production; PW_DIST_BACKEND=gloo lets several ranks
+    # share one GPU to exercise the multi-rank flow where only one GPU exists
+    backend = os.environ.get("PW_DIST_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # small scalar collectives
     lib = _abi.load()
 
     W = build_workload(cfg, rank, world, dev)
@@ -208,7 +215,7 @@ def run_ours(args, cfg):
             ids = search(p, mode)
             rec = builder.recall_at_k(ids, truth, k) if rank == 0 else 0.0
             if world > 1:
-                t = torch.tensor([rec], device=dev)
+                t = torch.tensor([rec], device=cdev)
                 dist.broadcast(t, 0)
                 rec = float(t.item())
             sweep.append((l, round(rec, 4)))
@@ -243,7 +250,7 @@ def run_ours(args, cfg):
         kern_ms = sum(a.elapsed_time(b) for a, b in timers) if with_timer else None
         launches = lib.pw_launch_count() - launches0
         if world > 1:
-            t = torch.tensor([ms], device=dev)
+            t = torch.tensor([ms], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, kern_ms, launches
@@ -285,7 +292,7 @@ def run_ours(args, cfg):
         res_host = eng.run_host(qhost, pw_params)
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev)
+        t = torch.tensor([e2e_s], device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     h2d = qhost.nbytes
@@ -306,6 +313,7 @@ def run_ours(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": cfg["workload"], "n": cfg["n"], "d": cfg["d"], "queries": nq,
                        "k": k, "degree": cfg["j"], "shards": world,
+                       "dist_backend": backend if world > 1 else None,
                        "arm": "pipelined path extension + ghost staging (rho=0.01) + direction-guided"
                               " selection (discard 0.5, cooldown 0.3)",
                        "l": ops["pathweaver"]["l"], "recall_at_10": ops["pathweaver"]["recall"],

@@ -76,6 +76,11 @@ class RingSearch:
         self.run_buf = dv.DeviceRun(q, world, k, self.dev)
         self.stream = torch.cuda.current_stream(self.dev)
         self._lib = None
+        self.gloo = False
+        if world > 1:
+            import torch.distributed as dist
+
+            self.gloo = dist.get_backend() == "gloo"
 
     # ---------------------------------------------------------------- device path
     def run(self, queries, params, mode: str, timer: list | None = None) -> np.ndarray | None:
@@ -118,6 +123,13 @@ class RingSearch:
             def send_recv(payload, next_q0, next_n):
                 # 4 B per query over NVLink (pipeline.py:339-341): NCCL P2P on the
                 # compute stream's order, so stage s+1 starts when its entries land
+                if self.gloo:  # host staging (gloo P2P is CPU-only)
+                    buf = torch.empty(next_n, dtype=torch.int32)
+                    reqs = [dist.isend(payload.cpu(), (g + 1) % N), dist.irecv(buf, (g - 1) % N)]
+                    for w in reqs:
+                        w.wait()
+                    ein[next_q0:next_q0 + next_n].copy_(buf)
+                    return
                 ops = [dist.P2POp(dist.isend, payload, (g + 1) % N),
                        dist.P2POp(dist.irecv, ein[next_q0:next_q0 + next_n], (g - 1) % N)]
                 for w in dist.batch_isend_irecv(ops):
@@ -127,10 +139,18 @@ class RingSearch:
         # all-gather this rank's column of the candidate lists, then reduce (K2)
         col_ids = R.shard_ids[:, g, :].contiguous()
         col_d = R.shard_dists[:, g, :].contiguous()
-        all_ids = torch.empty((N,) + tuple(col_ids.shape), dtype=col_ids.dtype, device=self.dev)
-        all_d = torch.empty((N,) + tuple(col_d.shape), dtype=col_d.dtype, device=self.dev)
-        dist.all_gather_into_tensor(all_ids, col_ids)
-        dist.all_gather_into_tensor(all_d, col_d)
+        if self.gloo:
+            li = [torch.empty_like(col_ids.cpu()) for _ in range(N)]
+            ld = [torch.empty_like(col_d.cpu()) for _ in range(N)]
+            dist.all_gather(li, col_ids.cpu())
+            dist.all_gather(ld, col_d.cpu())
+            all_ids = torch.stack(li).to(self.dev)
+            all_d = torch.stack(ld).to(self.dev)
+        else:
+            all_ids = torch.empty((N,) + tuple(col_ids.shape), dtype=col_ids.dtype, device=self.dev)
+            all_d = torch.empty((N,) + tuple(col_d.shape), dtype=col_d.dtype, device=self.dev)
+            dist.all_gather_into_tensor(all_ids, col_ids)
+            dist.all_gather_into_tensor(all_d, col_d)
         R.shard_ids.copy_(all_ids.permute(1, 0, 2))
         R.shard_dists.copy_(all_d.permute(1, 0, 2))
         dv.reduce(R, self.stream)
