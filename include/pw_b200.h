@@ -178,6 +178,11 @@ int pw_squared_l2_rows(pw_shard* shard, const int32_t* ids, int64_t n_ids,
 int pw_launch_config(pw_shard* shard, const pw_params* params, const pw_tuning* tuning,
                      int32_t* out6);
 
+/* Per-phase cycle totals of K1 summed over warps (init, score, merge,
+ * select, expand, dedup, visited, other) -- non-zero only in the
+ * PW_PHASE_TIMERS build (libpwb200_timers.so, tools/phase_timers.py). */
+int pw_phase_cycles(pw_shard* shard, int64_t* out8, int32_t reset);
+
 /* Number of kernel launches issued by this library since load (evidence for
  * bench.py's gpu_launches). */
 int64_t pw_launch_count(void);

@@ -81,8 +81,10 @@ EXPORTS = {
     "pw_squared_l2_rows": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p]),
     "pw_launch_config": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(Tuning), C.c_void_p]),
+    "pw_phase_cycles": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 }
 
+OPTIONAL = {"pw_phase_cycles", "pw_launch_config"}
 _LIB = None
 
 
@@ -96,7 +98,11 @@ def load(require_device: bool = True):
                 " (the CUDA extension is the only compute path; there is no CPU fallback)")
         lib = C.CDLL(str(LIB_PATH))
         for name, (res, args) in EXPORTS.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)
+            if fn is None:
+                if name in OPTIONAL:  # older builds loaded via PW_LIB for A/B runs
+                    continue
+                raise RuntimeError(f"{LIB_PATH} lacks {name}: rebuild it")
             fn.restype = res
             fn.argtypes = args
         _LIB = lib

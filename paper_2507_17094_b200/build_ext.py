@@ -51,28 +51,35 @@ def _run(cmd):
     return r.stderr
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> Path:
-    if not force and up_to_date():
-        return OUT
-    BUILD.mkdir(exist_ok=True)
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
+          timers: bool = False) -> Path:
+    """timers=True builds libpwb200_timers.so (K1 with per-phase clock64
+    counters, tools/phase_timers.py); the product library never has them."""
+    out = PKG / "libpwb200_timers.so" if timers else OUT
+    bdir = PKG / "_build_timers" if timers else BUILD
+    if not force and (out.exists() and all(p.stat().st_mtime <= out.stat().st_mtime for p in DEPS)):
+        return out
+    bdir.mkdir(exist_ok=True)
     nv = nvcc()
-    jobs_list = [([nv, *CFLAGS, "-c", str(CSRC / "pw_abi.cu"), "-o", str(BUILD / "pw_abi.o")],
-                  BUILD / "pw_abi.o")]
+    extra = ["-DPW_PHASE_TIMERS"] if timers else []
+    jobs_list = [([nv, *CFLAGS, *extra, "-c", str(CSRC / "pw_abi.cu"), "-o", str(bdir / "pw_abi.o")],
+                  bdir / "pw_abi.o")]
     for d in DIMS:
-        obj = BUILD / f"k_{d}.o"
-        jobs_list.append(([nv, *CFLAGS, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",
+        obj = bdir / f"k_{d}.o"
+        jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",
                            str(obj)], obj))
     workers = jobs or max(1, min(len(jobs_list), os.cpu_count() or 1))
     with ThreadPoolExecutor(workers) as pool:
         logs = list(pool.map(lambda j: _run(j[0]), jobs_list))
     objs = [str(o) for _, o in jobs_list]
-    _run([nv, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(OUT) + ".tmp", *objs])
-    os.replace(str(OUT) + ".tmp", OUT)
-    (PKG / "build_ptxas.log").write_text("\n".join(logs))
+    _run([nv, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(out) + ".tmp", *objs])
+    os.replace(str(out) + ".tmp", out)
+    if not timers:
+        (PKG / "build_ptxas.log").write_text("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, timers="--timers" in sys.argv))

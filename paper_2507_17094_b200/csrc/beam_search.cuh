@@ -98,6 +98,7 @@ struct KArgs {
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
     int32_t bulk_adj;       // adjacency / direction rows may use cp.async.bulk
     int32_t prefetch;       // L2-prefetch predicted parent rows
+    unsigned long long* phase;  // per-phase cycle totals (PW_PHASE_TIMERS builds only)
     int32_t vis_limit;      // smem visited entries before spilling to global
     unsigned long long* gvis;  // per-warp global visited spill tables, (epoch << 32 | id)
     int32_t gmask;
@@ -221,6 +222,17 @@ __device__ __forceinline__ float sqd(float x, float q) {
     return __fmul_rn(df, df);
 }
 
+// (x - q)^2 for two lanes of a float2 with packed sub.rn/mul.rn.f32x2 (SASS
+// FADD2/FMUL2; each half rounds exactly like the scalar __fsub_rn/__fmul_rn)
+__device__ __forceinline__ float2 sqd2(float2 x, float2 q) {
+    unsigned long long xv = *reinterpret_cast<const unsigned long long*>(&x);
+    unsigned long long qv = *reinterpret_cast<const unsigned long long*>(&q);
+    unsigned long long d, r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(xv), "l"(qv));
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(r) : "l"(d));
+    return *reinterpret_cast<const float2*>(&r);
+}
+
 // numpy pairwise_sum leaf over squared differences, lanes (v, a=lane&7)
 // hold accumulator a; every lane of the 8-lane group ends with the leaf sum.
 __device__ __forceinline__ float l2_leaf(const float* x, const float* q, int off, int len,
@@ -307,14 +319,15 @@ __device__ __forceinline__ float pw_leaf4(const float* x, const float* q, unsign
         constexpr int NF = N - (N % 8);
         const float2* x2 = reinterpret_cast<const float2*>(x + OFF);
         const float2* q2 = reinterpret_cast<const float2*>(q + OFF);
-        float2 xv = x2[c], qv = q2[c];
-        float r0 = sqd(xv.x, qv.x), r1 = sqd(xv.y, qv.y);
+        // packed FADD2/FMUL2 for (x - q)^2 on both accumulators; the adds stay
+        // scalar so ptxas cannot contract mul+add into FFMA2 (bit-exactness)
+        float2 sq = sqd2(x2[c], q2[c]);
+        float r0 = sq.x, r1 = sq.y;
 #pragma unroll
         for (int p = 1; p < NF / 8; p++) {
-            xv = x2[4 * p + c];
-            qv = q2[4 * p + c];
-            r0 = __fadd_rn(r0, sqd(xv.x, qv.x));
-            r1 = __fadd_rn(r1, sqd(xv.y, qv.y));
+            sq = sqd2(x2[4 * p + c], q2[4 * p + c]);
+            r0 = __fadd_rn(r0, sq.x);
+            r1 = __fadd_rn(r1, sq.y);
         }
         float a = __fadd_rn(r0, r1);
         a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
@@ -352,10 +365,8 @@ __device__ __forceinline__ float pw_sum(const float* x, const float* q, unsigned
 // --------------------------------------------------------------- per warp
 struct WarpState {
     float* q;
-    uint64_t* qk0;
-    uint64_t* qk1;
-    uint8_t* qe0;
-    uint8_t* qe1;
+    uint64_t* qk0;          // the size-l queue (keys, sorted) -- merged in place
+    uint8_t* qe0;           // expanded flags
     int32_t* cand;
     int32_t* cslot;
     int32_t* newl;
@@ -368,14 +379,15 @@ struct WarpState {
     unsigned long long* gvis;
     uint32_t* gscr;
     uint32_t epoch;         // this search's spill-table tag (0 never used)
+#ifdef PW_PHASE_TIMERS
+    long long pc[8];        // cycles: init, score, merge, select, expand, dedup, visited, tail
+#endif
     uint64_t* mbar;         // [0],[1] gather halves, [2] expansion fetch
     uint4* desc;            // bulk-copy descriptors of one expansion fetch (<= 32)
     uint32_t phase;         // parity bit per mbarrier
     int32_t cur;            // current queue buffer
-    __device__ __forceinline__ uint64_t* qk_cur() const { return cur ? qk1 : qk0; }
-    __device__ __forceinline__ uint64_t* qk_nxt() const { return cur ? qk0 : qk1; }
-    __device__ __forceinline__ uint8_t* qe_cur() const { return cur ? qe1 : qe0; }
-    __device__ __forceinline__ uint8_t* qe_nxt() const { return cur ? qe0 : qe1; }
+    __device__ __forceinline__ uint64_t* qk_cur() const { return qk0; }
+    __device__ __forceinline__ uint8_t* qe_cur() const { return qe0; }
     int32_t qlen;
     int32_t vcount;         // entries in the smem visited table
     bool ovf;               // visited set spilled to the global table
@@ -729,16 +741,18 @@ static __device__ __noinline__ void sort_survivors_smem(uint64_t* ckey, int s) {
 
 // search.py:170-190 merge_and_sort on keys; returns `inserted`.
 static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int n) {
+    // In place, single buffer: sort the survivors, find each one's insertion
+    // point P_i = lower_bound(queue, S_i), shift only the queue tail
+    // [min P_i, qlen) back to front (entry t moves to t + #{P_i <= t}; entries
+    // pushed past l fall off), then drop survivor i at P_i + i.  Keys are
+    // unique, so the positions form the merged order exactly.
     const unsigned lane = lane_id();
     const int L = C.L;
-    const uint64_t* qk = S.qk_cur();
-    const uint8_t* qe = S.qe_cur();
-    uint64_t* nk = S.qk_nxt();
-    uint8_t* ne = S.qe_nxt();
+    uint64_t* qk = S.qk0;
+    uint8_t* qe = S.qe0;
     const int qlen = S.qlen;
     const uint64_t thr = qlen == L ? qk[L - 1] : ~0ull;
-    // survivors (compacted in place in ckey)
-    int s = 0;
+    int s = 0;  // survivors (compacted in place in ckey)
     for (int base = 0; base < n; base += 32) {
         int t = base + lane;
         uint64_t key = t < n ? S.ckey[t] : ~0ull;
@@ -750,87 +764,57 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     }
     __syncwarp();
     if (s == 0) return 0;
-    if (s <= 256) {
-        // sort the survivors (warp bitonic, K per lane) into ckey[0..s), then
-        // merge-path positions by binary search on both sorted runs
-        if (s <= 32) {
-            uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
-            x = warp_sort_u64(x);
-            if ((int)lane < s) S.ckey[lane] = x;
-        } else {
-            sort_survivors_smem(S.ckey, s);
+    if (s <= 32) {
+        uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
+        x = warp_sort_u64(x);
+        if ((int)lane < s) S.ckey[lane] = x;
+    } else {
+        sort_survivors_smem(S.ckey, s);
+    }
+    __syncwarp();
+    int32_t* ppos = S.cslot;  // free during the merge
+    for (int i = lane; i < s; i += 32) {
+        const uint64_t key = S.ckey[i];
+        int lo = 0, hi = qlen;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (qk[mid] < key) lo = mid + 1;
+            else hi = mid;
         }
-        __syncwarp();
-        for (int t = lane; t < qlen; t += 32) {
-            const uint64_t key = qk[t];
-            int lo = 0, hi = s;  // survivors smaller than key
+        ppos[i] = lo;
+    }
+    __syncwarp();
+    const int pmin = ppos[0];
+    if (qlen > pmin) {
+        for (int base = pmin + ((qlen - 1 - pmin) >> 5) * 32; base >= pmin; base -= 32) {
+            const int t = base + (int)lane;
+            const bool valid = t < qlen;
+            const uint64_t key = valid ? qk[t] : 0ull;
+            const uint8_t fl = valid ? qe[t] : 0;
+            int lo = 0, hi = s;  // #{i : P_i <= t}
             while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (S.ckey[mid] < key) lo = mid + 1;
+                const int mid = (lo + hi) >> 1;
+                if (ppos[mid] <= t) lo = mid + 1;
                 else hi = mid;
             }
             const int np = t + lo;
-            if (np < L) {
-                nk[np] = key;
-                ne[np] = qe[t];
+            __syncwarp();
+            if (valid && np < L) {
+                qk[np] = key;
+                qe[np] = fl;
             }
-        }
-        int ins = 0;
-        for (int base = 0; base < s; base += 32) {
-            const int i = base + (int)lane;
-            bool kept = false;
-            if (i < s) {
-                const uint64_t mine = S.ckey[i];
-                int lo = 0, hi = qlen;
-                while (lo < hi) {
-                    int mid = (lo + hi) >> 1;
-                    if (qk[mid] < mine) lo = mid + 1;
-                    else hi = mid;
-                }
-                const int p = i + lo;
-                if (p < L) {
-                    nk[p] = mine;
-                    ne[p] = 0;
-                    kept = true;
-                }
-            }
-            ins += __popc(__ballot_sync(0xffffffffu, kept));
-        }
-        __syncwarp();
-        S.qlen = min(L, qlen + s);
-        S.cur ^= 1;
-        return ins;
-    }
-    // queue entries: shift by number of smaller survivors
-    for (int t = lane; t < qlen; t += 32) {
-        uint64_t key = qk[t];
-        int sh = 0;
-        for (int i = 0; i < s; i++) sh += S.ckey[i] < key;
-        int np = t + sh;
-        if (np < L) {
-            nk[np] = key;
-            ne[np] = qe[t];
+            __syncwarp();
         }
     }
-    // survivors: rank among survivors + lower_bound in the queue
     int ins = 0;
     for (int base = 0; base < s; base += 32) {
-        int i = base + lane;
+        const int i = base + (int)lane;
         bool kept = false;
         if (i < s) {
-            uint64_t key = S.ckey[i];
-            int rs = 0;
-            for (int o = 0; o < s; o++) rs += S.ckey[o] < key;
-            int lo = 0, hi = qlen;
-            while (lo < hi) {
-                int mid = (lo + hi) >> 1;
-                if (qk[mid] < key) lo = mid + 1;
-                else hi = mid;
-            }
-            int p = rs + lo;
+            const int p = ppos[i] + i;
             if (p < L) {
-                nk[p] = key;
-                ne[p] = 0;
+                qk[p] = S.ckey[i];
+                qe[p] = 0;
                 kept = true;
             }
         }
@@ -838,7 +822,6 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     }
     __syncwarp();
     S.qlen = min(L, qlen + s);
-    S.cur ^= 1;
     return ins;
 }
 
@@ -1112,6 +1095,23 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
     return np * nsel;
 }
 
+#ifdef PW_PHASE_TIMERS
+#define PW_T0() long long pw_t_ = clock64()
+#define PW_T(i)                          \
+    do {                                 \
+        const long long n_ = clock64();  \
+        S.pc[i] += n_ - pw_t_;           \
+        pw_t_ = n_;                      \
+    } while (0)
+#else
+#define PW_T0() \
+    do {        \
+    } while (0)
+#define PW_T(i) \
+    do {        \
+    } while (0)
+#endif
+
 // One full search (search.py:269-335) over graph G.  Seeds (already in
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
@@ -1120,6 +1120,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
                            int ns, bool fill_random, Pcg64& rng, int64_t task,
                            int64_t* n_logged) {
     const unsigned lane = lane_id();
+    PW_T0();
     // reset per-search state
     if (D == 0)
         for (int i = lane; i < A.H; i += 32) S.vh[i] = kEmpty;
@@ -1166,6 +1167,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     }
     bh_clear(A, S);
     int n_new = visited_filter<(D > 0)>(A, S, nb);
+    PW_T(0);
 
     bool converged = false;
     int32_t* parents = S.misc + A.PG * G.j + A.PG * A.W + 8;
@@ -1182,8 +1184,11 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
                 *n_logged += n_new;
             }
             S.c_dc += n_new;
+            PW_T(7);
             score_rows<D>(A, S, G, n_new);
+            PW_T(1);
             inserted = merge_queue(A, S, C, n_new);
+            PW_T(2);
             S.c_ins += inserted;
         }
         if (inserted == 0) {
@@ -1192,17 +1197,22 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         }
         if (it == C.max_iter - 1) break;
         int np = select_parents(S, C.r, parents);
+        PW_T(3);
         if (np == 0) {
             converged = true;
             break;
         }
         S.c_ne += np;
         int nc = expand<D>(A, S, G, C, parents, np, it, rng);
+        PW_T(4);
         nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
         S.c_tv += nb;
         bh_clear(A, S);
+        PW_T(5);
         n_new = visited_filter<(D > 0)>(A, S, nb);
+        PW_T(6);
     }
+    PW_T(7);
     return converged;
 }
 
@@ -1216,9 +1226,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
     WarpState S;
     S.q = reinterpret_cast<float*>(base + A.o_q);
     S.qk0 = reinterpret_cast<uint64_t*>(base + A.o_qk);
-    S.qk1 = S.qk0 + A.L_max;
     S.qe0 = reinterpret_cast<uint8_t*>(base + A.o_qe);
-    S.qe1 = S.qe0 + A.L_max;
     S.cand = reinterpret_cast<int32_t*>(base + A.o_cand);
     S.cslot = reinterpret_cast<int32_t*>(base + A.o_cslot);
     S.newl = reinterpret_cast<int32_t*>(base + A.o_newl);
@@ -1230,6 +1238,9 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
     S.misc = reinterpret_cast<int32_t*>(base + A.o_misc);
     S.gvis = A.gvis + (size_t)gwarp * (A.gmask + 1);
     S.epoch = A.gepoch[gwarp];
+#ifdef PW_PHASE_TIMERS
+    for (int i = 0; i < 8; i++) S.pc[i] = 0;
+#endif
     S.gscr = A.gscratch + (size_t)gwarp * A.gscratch_words;
     S.mbar = reinterpret_cast<uint64_t*>(base + A.o_mbar);
     S.desc = reinterpret_cast<uint4*>(base + A.o_desc);
@@ -1342,6 +1353,10 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         __syncwarp();
     }
     if (lane == 0) A.gepoch[gwarp] = S.epoch;
+#ifdef PW_PHASE_TIMERS
+    if (lane == 0)
+        for (int i = 0; i < 8; i++) atomicAdd(A.phase + i, (unsigned long long)S.pc[i]);
+#endif
 }
 
 typedef void (*KernelFn)(KArgs);

@@ -149,6 +149,7 @@ struct pw_shard {
     int64_t bytes = 0;
     // launch workspace (grow-only)
     int32_t* counter = nullptr;
+    unsigned long long* phase = nullptr;  // 8 cycle counters (timer builds)
     unsigned long long* gvis = nullptr;
     size_t gvis_words = 0;
     uint32_t* gepoch = nullptr;
@@ -377,8 +378,8 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
     int64_t off = 0;
     A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
-    A.o_qk = (int32_t)off; off = al(off + 8 * 2 * (int64_t)p.l);
-    A.o_qe = (int32_t)off; off = al(off + 2 * (int64_t)p.l);
+    A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
+    A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
     A.o_cand = (int32_t)off; off = al(off + 4 * cb);
     A.o_cslot = (int32_t)off; off = al(off + 4 * cb);
     A.o_newl = (int32_t)off; off = al(off + 4 * cb);
@@ -426,7 +427,10 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     if (!sh->counter) {
         PW_CUDA(cudaMalloc(&sh->counter, sizeof(int32_t) * 2));
         PW_CUDA(cudaMemset(sh->counter, 0, sizeof(int32_t) * 2));
+        PW_CUDA(cudaMalloc(&sh->phase, sizeof(unsigned long long) * 8));
+        PW_CUDA(cudaMemset(sh->phase, 0, sizeof(unsigned long long) * 8));
     }
+    A.phase = sh->phase;
     if (sh->gvis_words < (size_t)total_warps * gsz || sh->gepoch_n < (size_t)total_warps) {
         // epoch-tagged tables: zero once (epoch 0 is never used by a search)
         if (sh->gvis) cudaFree(sh->gvis);
@@ -546,7 +550,7 @@ int pw_shard_destroy(pw_shard* sh) {
     cudaGetDevice(&cur);
     cudaSetDevice(sh->device);
     void* ptrs[] = {sh->vec, sh->adj, sh->gid, sh->dir, sh->inter, sh->gvec, sh->gadj, sh->gids,
-                    sh->counter, sh->gvis, sh->gscr, sh->gepoch};
+                    sh->counter, sh->gvis, sh->gscr, sh->gepoch, sh->phase};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     cudaSetDevice(cur);
@@ -825,6 +829,17 @@ int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, cons
     }
     cudaFree(buf);
     return rc;
+}
+
+int pw_phase_cycles(pw_shard* sh, int64_t* out8, int32_t reset) {
+    if (!sh || !out8) return set_err(PW_EINVAL, "null argument");
+    for (int i = 0; i < 8; i++) out8[i] = 0;
+    if (!sh->phase) return 0;
+    PW_CUDA(cudaSetDevice(sh->device));
+    PW_CUDA(cudaDeviceSynchronize());
+    PW_CUDA(cudaMemcpy(out8, sh->phase, sizeof(int64_t) * 8, cudaMemcpyDeviceToHost));
+    if (reset) PW_CUDA(cudaMemset(sh->phase, 0, sizeof(unsigned long long) * 8));
+    return 0;
 }
 
 int pw_launch_config(pw_shard* sh, const pw_params* params, const pw_tuning* tuning,

@@ -47,7 +47,10 @@ for tuning in tunings:
         ms = sum(a.elapsed_time(b) for a, b in timer) / args.reps
         st = run.stats()[0]
         from paper_2507_17094_b200 import _abi
-        lc = _abi.launch_config(shard.handle, p, tuning)
+        try:
+            lc = _abi.launch_config(shard.handle, p, tuning)
+        except AttributeError:
+            lc = {"warps_per_sm": None, "smem_per_warp": None}
         out[arm] = dict(kernel_ms=round(ms, 3), qps=round(q.shape[0] / ms * 1e3),
                         warps=lc["warps_per_sm"], smem=lc["smem_per_warp"],
                         dc=float(st["distance_computations"].mean()), it=float(st["iterations"].mean()))

@@ -1,2 +1,6 @@
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-PW_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --config c2s --steps 4 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; tail -5 gpurun_out/bench_n2.err; cat gpurun_out/bench_n2.json
+timeout 600 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
+for i in 1 2; do
+PW_LIB=tools/lib_prev.so timeout 900 python tools/ab.py --config c2 --l 256 2>>gpurun_out/ab.err >> gpurun_out/ab.log
+timeout 900 python tools/ab.py --config c2 --l 256 2>>gpurun_out/ab.err >> gpurun_out/ab.log
+done
+cat gpurun_out/ab.log
