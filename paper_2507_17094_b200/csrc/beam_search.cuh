@@ -527,7 +527,7 @@ static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint3
         }
         g = (g + 1u) & gm;
         gp++;
-        cur = gvis[g];
+        cur = __ldcg(&gvis[g]);
     }
     atomicOr(err, 8);  // global visited table full
     return false;
@@ -565,7 +565,7 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
     const uint32_t gm = (uint32_t)A.gmask;
     for (int base0 = 0; base0 < nb; base0 += 32 * K) {
         int32_t id[K];
-        uint32_t slot[K];
+        uint32_t slot[K], sh[K];
         unsigned long long v[K];
         bool pend[K], fresh[K];
 #pragma unroll
@@ -574,34 +574,36 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
             id[k] = t < nb ? S.newl[t] : -1;
             pend[k] = t < nb && (GLOBAL_ONLY || !smem_lookup(A, S, (uint32_t)id[k]));
             slot[k] = (hash32((uint32_t)id[k] ^ 0x5bd1e995u) >> 3) & gm;
-            v[k] = pend[k] ? S.gvis[slot[k]] : 0ull;
+            // count how many candidates of this batch share a home slot
+            // (shared-memory hash; the ordered-dedup table is free here)
+            sh[k] = pend[k] ? bh_insert(A, S, slot[k]) : 0u;
+            if (pend[k]) atomicAdd(&S.bhp[sh[k]], 1);
+            v[k] = pend[k] ? __ldcg(&S.gvis[slot[k]]) : 0ull;  // one round trip for all
             fresh[k] = false;
         }
-        // one CAS per stale first slot, all in flight together
-        unsigned long long old[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            const unsigned long long want = ((unsigned long long)S.epoch << 32) | (uint32_t)id[k];
-            old[k] = v[k];
-            if (pend[k] && v[k] != want && (uint32_t)(v[k] >> 32) != S.epoch)
-                old[k] = atomicCAS(&S.gvis[slot[k]], v[k], want);
-        }
+        __syncwarp();
+        // fast path: a stale home slot claimed by exactly one candidate gets a
+        // plain (fire-and-forget) store; found == already visited
 #pragma unroll
         for (int k = 0; k < K; k++) {
             if (!pend[k]) continue;
             const unsigned long long want = ((unsigned long long)S.epoch << 32) | (uint32_t)id[k];
-            if (old[k] == want) {                       // already visited (or lost a same-id race)
+            const bool alone = (uint32_t)S.bhp[sh[k]] == 0x80000000u;  // 0x7FFFFFFF + one add
+            if (v[k] == want) {
                 pend[k] = false;
-            } else if (old[k] == v[k] && (uint32_t)(v[k] >> 32) != S.epoch) {
-                pend[k] = false;                        // our CAS claimed the stale slot
+            } else if (alone && (uint32_t)(v[k] >> 32) != S.epoch) {
+                __stcg(&S.gvis[slot[k]], want);
+                pend[k] = false;
                 fresh[k] = true;
             }
         }
-        // collisions: linear probing from the next slot (load factor <= 1/2)
+        __syncwarp();  // the plain stores are ordered before any CAS below
+        // slow path (occupied or shared home slot): CAS + linear probing
 #pragma unroll
         for (int k = 0; k < K; k++)
             if (pend[k])
-                fresh[k] = probe_insert(S.gvis, gm, S.epoch, (uint32_t)id[k], slot[k], old[k], A.err);
+                fresh[k] = probe_insert(S.gvis, gm, S.epoch, (uint32_t)id[k], slot[k],
+                                        __ldcg(&S.gvis[slot[k]]), A.err);
 #pragma unroll
         for (int k = 0; k < K; k++) {
             const unsigned b = __ballot_sync(0xffffffffu, fresh[k]);
@@ -609,6 +611,7 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
             if (fresh[k]) S.newl[pos] = id[k];
             cnt += __popc(b);
         }
+        bh_clear(A, S);
     }
     __syncwarp();
     return cnt;
