@@ -93,6 +93,8 @@ struct KArgs {
     int64_t visit_cap;
     // per-warp shared-memory layout (bytes)
     int32_t L_max, CB, BH, H, R, PG;
+    int32_t pstride;        // DGS parent-row stride in floats (16-byte multiple)
+    int32_t o_par;          // parents list offset in misc (words)
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
         o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
@@ -187,6 +189,38 @@ __device__ __forceinline__ uint64_t warp_sort_u64(uint64_t x) {
             x = keep_min ? (o < x ? o : x) : (o > x ? o : x);
         }
     return x;
+}
+// 64 keys, element i = 32*e + lane in register x[e]: bitonic network with
+// the j = 32 stage as an in-lane compare-exchange (ascending across i)
+__device__ __forceinline__ void warp_sort2_u64(uint64_t& x0, uint64_t& x1) {
+    const unsigned lane = threadIdx.x & 31u;
+#pragma unroll 1
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll 1
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            // element lane ascends iff (lane & k) == 0; element 32 + lane has
+            // the k = 32 bit set, so it descends at k = 32 (bitonic 64)
+            const uint64_t o0 = __shfl_xor_sync(0xffffffffu, x0, j);
+            const uint64_t o1 = __shfl_xor_sync(0xffffffffu, x1, j);
+            const bool lo = (lane & j) == 0;
+            const bool asc0 = (lane & k) == 0;
+            const bool asc1 = k == 32 ? false : asc0;
+            x0 = (lo == asc0) ? (o0 < x0 ? o0 : x0) : (o0 > x0 ? o0 : x0);
+            x1 = (lo == asc1) ? (o1 < x1 ? o1 : x1) : (o1 > x1 ? o1 : x1);
+        }
+    {
+        const uint64_t a = x0 < x1 ? x0 : x1, b = x0 < x1 ? x1 : x0;
+        x0 = a;
+        x1 = b;
+    }
+#pragma unroll 1
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint64_t o0 = __shfl_xor_sync(0xffffffffu, x0, j);
+        const uint64_t o1 = __shfl_xor_sync(0xffffffffu, x1, j);
+        const bool lo = (lane & j) == 0;
+        x0 = lo ? (o0 < x0 ? o0 : x0) : (o0 > x0 ? o0 : x0);
+        x1 = lo ? (o1 < x1 ? o1 : x1) : (o1 > x1 ? o1 : x1);
+    }
 }
 __device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
     const unsigned lane = threadIdx.x & 31u;
@@ -389,6 +423,7 @@ struct WarpState {
     __device__ __forceinline__ uint64_t* qk_cur() const { return qk0; }
     __device__ __forceinline__ uint8_t* qe_cur() const { return qe0; }
     int32_t qlen;
+    int32_t fu;             // first queue position that may be unexpanded
     int32_t vcount;         // entries in the smem visited table
     bool ovf;               // visited set spilled to the global table
     int64_t c_it, c_dc, c_tv, c_ne, c_dgs, c_ins;
@@ -455,6 +490,43 @@ static __device__ int dedup_ordered(const KArgs& A, WarpState& S, const int32_t*
     __syncwarp();
     *n_unique = cnt;
     return cnt < limit ? cnt : limit;
+}
+
+// Same set and count as dedup_ordered when nothing is truncated (n <= cap)
+// and no visit log is kept: order inside the batch does not change any result
+// (scores are merged by key), so one CAS pass with two candidates in flight
+// per lane replaces insert + atomicMin + the ordered second pass.  Needs a
+// clear bhk; leaves it populated.
+static __device__ int dedup_unordered(const KArgs& A, WarpState& S, const int32_t* src, int n,
+                                      int32_t* dst) {
+    const unsigned lane = lane_id();
+    const uint32_t mask = (uint32_t)A.BH - 1u;
+    int cnt = 0;
+    for (int base = 0; base < n; base += 64) {
+        const int t0 = base + (int)lane, t1 = t0 + 32;
+        // idle lanes: o == id (not kEmpty) skips the probe loop and the ballot
+        const uint32_t id0 = t0 < n ? (uint32_t)src[t0] : 0u;
+        const uint32_t id1 = t1 < n ? (uint32_t)src[t1] : 0u;
+        uint32_t h0 = hash32(id0) & mask, h1 = hash32(id1) & mask;
+        uint32_t o0 = t0 < n ? atomicCAS(&S.bhk[h0], kEmpty, id0) : id0;
+        uint32_t o1 = t1 < n ? atomicCAS(&S.bhk[h1], kEmpty, id1) : id1;
+        while (o0 != kEmpty && o0 != id0) {
+            h0 = (h0 + 1u) & mask;
+            o0 = atomicCAS(&S.bhk[h0], kEmpty, id0);
+        }
+        while (o1 != kEmpty && o1 != id1) {
+            h1 = (h1 + 1u) & mask;
+            o1 = atomicCAS(&S.bhk[h1], kEmpty, id1);
+        }
+        const unsigned b0 = __ballot_sync(0xffffffffu, o0 == kEmpty);
+        const unsigned b1 = __ballot_sync(0xffffffffu, o1 == kEmpty);
+        if (o0 == kEmpty) dst[cnt + __popc(b0 & lanemask_lt())] = (int32_t)id0;
+        cnt += __popc(b0);
+        if (o1 == kEmpty) dst[cnt + __popc(b1 & lanemask_lt())] = (int32_t)id1;
+        cnt += __popc(b1);
+    }
+    __syncwarp();
+    return cnt;
 }
 
 // Exact visited-set insert-if-absent (search.py:167, :300-303).
@@ -771,40 +843,75 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
         uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
         x = warp_sort_u64(x);
         if ((int)lane < s) S.ckey[lane] = x;
+    } else if (s <= 64) {
+        uint64_t x0 = S.ckey[lane];
+        uint64_t x1 = 32 + (int)lane < s ? S.ckey[32 + lane] : ~0ull;
+        warp_sort2_u64(x0, x1);
+        S.ckey[lane] = x0;
+        if (32 + (int)lane < s) S.ckey[32 + lane] = x1;
     } else {
         sort_survivors_smem(S.ckey, s);
     }
     __syncwarp();
-    int32_t* ppos = S.cslot;  // free during the merge
-    for (int i = lane; i < s; i += 32) {
-        const uint64_t key = S.ckey[i];
-        int lo = 0, hi = qlen;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (qk[mid] < key) lo = mid + 1;
-            else hi = mid;
+    int32_t* ppos = S.newl;  // free once scoring has turned ids into keys
+    // P_i = lower_bound(queue, S_i): branch-free bit descent, two searches in
+    // flight per lane
+    int qstep = 1;
+    while (qstep <= qlen) qstep <<= 1;
+    qstep >>= 1;
+    for (int i0 = lane; i0 < s; i0 += 64) {
+        const int i1 = i0 + 32;
+        const uint64_t k0 = S.ckey[i0];
+        const uint64_t k1 = i1 < s ? S.ckey[i1] : 0ull;
+        int p0 = 0, p1 = 0;
+        for (int st = qstep; st > 0; st >>= 1) {
+            if (p0 + st <= qlen && qk[p0 + st - 1] < k0) p0 += st;
+            if (p1 + st <= qlen && qk[p1 + st - 1] < k1) p1 += st;
         }
-        ppos[i] = lo;
+        ppos[i0] = p0;
+        if (i1 < s) ppos[i1] = p1;
     }
     __syncwarp();
     const int pmin = ppos[0];
+    S.fu = min(S.fu, pmin);  // entries before pmin keep their place (and flags)
     if (qlen > pmin) {
-        for (int base = pmin + ((qlen - 1 - pmin) >> 5) * 32; base >= pmin; base -= 32) {
-            const int t = base + (int)lane;
-            const bool valid = t < qlen;
-            const uint64_t key = valid ? qk[t] : 0ull;
-            const uint8_t fl = valid ? qe[t] : 0;
-            int lo = 0, hi = s;  // #{i : P_i <= t}
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (ppos[mid] <= t) lo = mid + 1;
-                else hi = mid;
+        // Queue tail [pmin, qlen): entry t moves to t + #{i : P_i <= t}.  Up to
+        // 8 chunks are read into registers, their targets found with
+        // independent bit-descent searches over ppos, then written -- back to
+        // front by 256-entry groups, so every write lands on an entry that was
+        // already read (targets are distinct and >= the source).
+        int sstep = 1;
+        while (sstep <= s) sstep <<= 1;
+        sstep >>= 1;
+        for (int g_end = qlen; g_end > pmin; g_end -= 256) {
+            const int g0 = max(pmin, g_end - 256);
+            uint64_t key[8];
+            int np[8];
+            uint32_t fl = 0;
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int t = g0 + 32 * c + (int)lane;
+                const bool valid = t < g_end;
+                key[c] = valid ? qk[t] : 0ull;
+                fl |= (valid && qe[t]) ? (1u << c) : 0u;
+                np[c] = 0;
             }
-            const int np = t + lo;
+            for (int st = sstep; st > 0; st >>= 1) {
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    const int t = g0 + 32 * c + (int)lane;
+                    if (np[c] + st <= s && ppos[np[c] + st - 1] <= t) np[c] += st;
+                }
+            }
             __syncwarp();
-            if (valid && np < L) {
-                qk[np] = key;
-                qe[np] = fl;
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const int t = g0 + 32 * c + (int)lane;
+                const int dst = t + np[c];
+                if (t < g_end && dst < L) {
+                    qk[dst] = key[c];
+                    qe[dst] = (uint8_t)((fl >> c) & 1u);
+                }
             }
             __syncwarp();
         }
@@ -829,12 +936,14 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
 }
 
 // search.py:192-204: first r unexpanded queue entries, marked expanded.
+// S.fu: every entry before it is expanded (merges lower it to their first
+// insertion point), so the scan starts at its chunk.
 static __device__ int select_parents(WarpState& S, int r, int32_t* parents) {
     const unsigned lane = lane_id();
     uint64_t* qk = S.qk_cur();
     uint8_t* qe = S.qe_cur();
-    int np = 0;
-    for (int base = 0; base < S.qlen && np < r; base += 32) {
+    int np = 0, last = -1;
+    for (int base = S.fu & ~31; base < S.qlen && np < r; base += 32) {
         int t = base + lane;
         bool f = t < S.qlen && qe[t] == 0;
         unsigned b = __ballot_sync(0xffffffffu, f);
@@ -843,8 +952,11 @@ static __device__ int select_parents(WarpState& S, int r, int32_t* parents) {
             parents[pos] = (int32_t)(uint32_t)qk[t];
             qe[t] = 1;
         }
+        const unsigned lb = __ballot_sync(0xffffffffu, f && pos == r - 1);
+        if (lb) last = base + __ffs(lb) - 1;
         np = min(r, np + __popc(b));
     }
+    S.fu = np == r ? last + 1 : S.qlen;
     __syncwarp();
     return np;
 }
@@ -981,7 +1093,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
         for (int pg = 0; pg < np; pg += A.PG) {
             const int gp = min(A.PG, np - pg);
             float* prow = S.stage;
-            uint32_t* drow = reinterpret_cast<uint32_t*>(S.stage + (size_t)gp * A.spad);
+            uint32_t* drow = reinterpret_cast<uint32_t*>(S.stage + (size_t)gp * A.pstride);
             fetch_group(A, S, 3 * gp, gp * (adj_bytes + vec_bytes + dir_bytes),
                         [&](int r, void*& dst, const void*& src, uint32_t& b) {
                             const int pi = r % gp, kind = r / gp;
@@ -991,7 +1103,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                                 src = G.adj + (size_t)par * j;
                                 b = adj_bytes;
                             } else if (kind == 1) {
-                                dst = prow + (size_t)pi * A.spad;
+                                dst = prow + (size_t)pi * A.pstride;
                                 src = G.vec + (size_t)par * d;
                                 b = vec_bytes;
                             } else {
@@ -1010,7 +1122,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
 #pragma unroll
                     for (int w = 0; w < WC; w++) {
                         const int t = 32 * w + (int)lane;
-                        const bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
+                        const bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.pstride + t];
                         qb[w] = __ballot_sync(0xffffffffu, bit);
                     }
                     int c = 0;
@@ -1055,7 +1167,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                 for (int pi = 0; pi < gp; pi++)
                     for (int w = 0; w < W; w++) {
                         int t = 32 * w + (int)lane;
-                        bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.spad + t];
+                        bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.pstride + t];
                         unsigned word = __ballot_sync(0xffffffffu, bit);
                         if (lane == 0) qb[pi * W + w] = word;
                     }
@@ -1130,6 +1242,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     bh_clear(A, S);
     S.cur = 0;
     S.qlen = 0;
+    S.fu = 0;
     S.vcount = 0;
     S.ovf = false;
     S.epoch = S.epoch == 0xFFFFFFFFu ? 1u : S.epoch + 1u;
@@ -1148,8 +1261,9 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
                 rng = choice_tail(rng, pop, size, S.gscr, S.gscr + cap, cap - 1, ch);
             } else {
                 uint32_t mask = (uint32_t)gen_mask64((uint64_t)(1.2 * (double)size));
-                uint32_t* set = ((int64_t)(mask + 1) * 4 <= (int64_t)A.R * A.spad * 4)
-                                    ? reinterpret_cast<uint32_t*>(S.stage)
+                // ckey is free during the initial batch (stage aliases the dedup hash)
+                uint32_t* set = ((int64_t)(mask + 1) * 8 <= 8ll * max(64, A.CB))
+                                    ? reinterpret_cast<uint32_t*>(S.ckey)
                                     : S.gscr;
                 rng = choice_floyd(rng, pop, size, set, mask, ch);
             }
@@ -1173,7 +1287,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     PW_T(0);
 
     bool converged = false;
-    int32_t* parents = S.misc + A.PG * G.j + A.PG * A.W + 8;
+    int32_t* parents = S.misc + A.o_par;
     for (int it = 0; it < C.max_iter; it++) {
         S.c_it++;
         int inserted = 0;
@@ -1208,7 +1322,11 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         S.c_ne += np;
         int nc = expand<D>(A, S, G, C, parents, np, it, rng);
         PW_T(4);
-        nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
+        bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
+        if (nc <= C.cap && !C.log)
+            nb = dedup_unordered(A, S, S.cand, nc, S.newl);
+        else
+            nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
         S.c_tv += nb;
         bh_clear(A, S);
         PW_T(5);

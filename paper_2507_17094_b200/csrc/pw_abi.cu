@@ -368,28 +368,45 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     if (R < 2) R = 2;
     int W = sh->W;
     int PG = 1;
+    // DGS parent rows are packed at a 16-byte stride (bit tests only, no
+    // bank-conflict concern) so that kParentGroup parents fit the staging
+    // ring and one expansion is ONE fetch round trip (C2: 8 x (96 + 96) words)
+    const int pstride = (d + 3) & ~3;
     if (A.cfg.prune_sel == PW_SEL_DIRECTION) {
-        while ((int64_t)R * spad < (int64_t)spad + (int64_t)G.j * W) R += 2;
-        PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad) / (spad + (int64_t)G.j * W));
+        while ((int64_t)R * spad < (int64_t)pstride + (int64_t)G.j * W) R += 2;
+        PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad) / (pstride + (int64_t)G.j * W));
         PG = std::max(PG, 1);
     }
     A.R = R;
     A.PG = PG;
+    A.pstride = pstride;
+    // The in-batch dedup hash (bhk/bhp) and its slot list (cslot) are live only
+    // between expansion and the visited filter, the staging ring only in
+    // scoring and DGS expansion (before the dedup): they share one region.
+    const int64_t hash_bytes = 8 * (int64_t)A.BH + 4 * cb;
+    const int64_t stage_bytes = std::max<int64_t>(4 * (int64_t)R * spad, hash_bytes);
+    // specialised kernels with j <= 32 keep the DGS counts/bits in registers
+    const bool dgs_regs = specialised && G.j <= 32;
     auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
     int64_t off = 0;
     A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
     A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
     A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
     A.o_cand = (int32_t)off; off = al(off + 4 * cb);
-    A.o_cslot = (int32_t)off; off = al(off + 4 * cb);
     A.o_newl = (int32_t)off; off = al(off + 4 * cb);
     A.o_ckey = (int32_t)off; off = al(off + 8 * std::max<int64_t>(64, next_pow2(cb)));  // pow2 for the survivor sort
-    A.o_bhk = (int32_t)off; off = al(off + 4 * (int64_t)A.BH);
-    A.o_bhp = (int32_t)off; off = al(off + 4 * (int64_t)A.BH);
     A.o_vh = (int32_t)off; off = al(off + 4 * H);
-    A.o_stage = (int32_t)off; off = al(off + 4 * (int64_t)R * spad);
+    A.o_stage = (int32_t)off;
+    A.o_bhk = (int32_t)off;
+    A.o_bhp = (int32_t)(off + 4 * (int64_t)A.BH);
+    A.o_cslot = (int32_t)(off + 8 * (int64_t)A.BH);
+    off = al(off + stage_bytes);
     A.o_misc = (int32_t)off;
-    int64_t misc = (int64_t)std::max(jm, PG * jm) + (int64_t)PG * W + 8 + p.r + 8;
+    // misc words: [DGS counts PG*j | perm j] [DGS bits PG*W] 8 pad | parents r | 8 pad
+    const int64_t misc_cnt = dgs_regs ? (int64_t)jm : (int64_t)std::max(jm, PG * jm);
+    const int64_t misc_bits = dgs_regs ? 0 : (int64_t)PG * W;
+    A.o_par = (int32_t)(misc_cnt + misc_bits + 8);
+    int64_t misc = misc_cnt + misc_bits + 8 + p.r + 8;
     off = al(off + 4 * misc);
     A.o_mbar = (int32_t)off;
     off = al(off + 3 * 8);
