@@ -104,6 +104,8 @@ struct KArgs {
     int32_t vis_limit;      // smem visited entries before spilling to global
     unsigned long long* gvis;  // per-warp global visited spill tables, (epoch << 32 | id)
     int32_t gmask;
+    int32_t lossy;          // lossy visited cache instead of the exact set (ids exact; DC may grow)
+    int32_t lshift;         // lossy cache slot = hash32(id) >> lshift
     uint32_t* gepoch;       // per-warp search epoch (tags the spill table; no clearing)
     uint32_t* gscratch;     // per-warp global scratch for choice()
     int64_t gscratch_words;
@@ -605,6 +607,44 @@ static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint3
     return false;
 }
 
+// Lossy visited filter (tuning flag 2): a per-warp direct-mapped cache of
+// (epoch8 << 24 | id) words in global memory, small enough to stay in L2
+// (8192 slots = 32 KB per warp).  One round trip, no atomics: every miss is
+// stored (overwrites allowed) and scored.  Results stay identical to the
+// exact set: a forgotten node that is re-scored either is still queued --
+// the merge finds its identical key and drops it -- or was dropped from /
+// never entered the queue, so its key is above the (non-increasing) l-th key
+// and it cannot survive.  Only distance_computations can exceed the
+// reference's.  A hit is never false: tags are unique per search and the
+// cache is cleared when the 8-bit epoch wraps.
+static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S, int nb) {
+    const unsigned lane = lane_id();
+    uint32_t* tab = reinterpret_cast<uint32_t*>(S.gvis);
+    const uint32_t tag = S.epoch << 24;
+    constexpr int K = 8;
+    int cnt = 0;
+    for (int base0 = 0; base0 < nb; base0 += 32 * K) {
+        uint32_t id[K], v[K];
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const int t = base0 + k * 32 + (int)lane;
+            id[k] = t < nb ? (uint32_t)S.newl[t] : 0u;
+            v[k] = t < nb ? __ldcg(&tab[hash32(id[k]) >> A.lshift]) : (tag | id[k]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+            const bool fresh = v[k] != (tag | id[k]);
+            if (fresh) __stcg(&tab[hash32(id[k]) >> A.lshift], tag | id[k]);
+            const unsigned b = __ballot_sync(0xffffffffu, fresh);
+            if (fresh) S.newl[cnt + __popc(b & lanemask_lt())] = (int32_t)id[k];
+            cnt += __popc(b);
+        }
+    }
+    __syncwarp();
+    return cnt;
+}
+
 // Keep only never-scored ids of newl[0..nb) (in order); returns n_new.
 // Until the shared-memory table would pass vis_limit, inserts go there
 // (one CAS each, no global traffic).  After the spill, every candidate not in
@@ -616,6 +656,7 @@ static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint3
 // is compiled into the hot loop.
 template <bool GLOBAL_ONLY>
 __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
+    if (A.lossy) return visited_lossy(A, S, nb);
     const unsigned lane = lane_id();
     if (!GLOBAL_ONLY && !S.ovf && S.vcount + nb > A.vis_limit) S.ovf = true;
     int cnt = 0;
@@ -859,6 +900,7 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     int qstep = 1;
     while (qstep <= qlen) qstep <<= 1;
     qstep >>= 1;
+    bool dup = false;
     for (int i0 = lane; i0 < s; i0 += 64) {
         const int i1 = i0 + 32;
         const uint64_t k0 = S.ckey[i0];
@@ -868,8 +910,33 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
             if (p0 + st <= qlen && qk[p0 + st - 1] < k0) p0 += st;
             if (p1 + st <= qlen && qk[p1 + st - 1] < k1) p1 += st;
         }
-        ppos[i0] = p0;
-        if (i1 < s) ppos[i1] = p1;
+        // lossy visited mode re-scores forgotten nodes: one still queued has
+        // the identical key (search.py:181 skips queued ids)
+        const bool d0 = p0 < qlen && qk[p0] == k0;
+        const bool d1 = i1 < s && p1 < qlen && qk[p1] == k1;
+        dup |= d0 | d1;
+        ppos[i0] = d0 ? -1 : p0;
+        if (i1 < s) ppos[i1] = d1 ? -1 : p1;
+    }
+    if (__any_sync(0xffffffffu, dup)) {
+        __syncwarp();
+        int s2 = 0;  // in-place compaction (each chunk is read before it is written)
+        for (int base = 0; base < s; base += 32) {
+            const int i = base + (int)lane;
+            const uint64_t key = i < s ? S.ckey[i] : 0ull;
+            const int pp = i < s ? ppos[i] : -1;
+            const unsigned b = __ballot_sync(0xffffffffu, pp >= 0);
+            __syncwarp();
+            if (pp >= 0) {
+                const int o = s2 + __popc(b & lanemask_lt());
+                S.ckey[o] = key;
+                ppos[o] = pp;
+            }
+            s2 += __popc(b);
+        }
+        s = s2;
+        __syncwarp();
+        if (s == 0) return 0;
     }
     __syncwarp();
     const int pmin = ppos[0];
@@ -1245,7 +1312,19 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     S.fu = 0;
     S.vcount = 0;
     S.ovf = false;
-    S.epoch = S.epoch == 0xFFFFFFFFu ? 1u : S.epoch + 1u;
+    if (A.lossy) {
+        // 8-bit tags 1..255; on wrap the cache is cleared (tag 0 = never used)
+        if (++S.epoch > 255u) {
+            uint4* t4 = reinterpret_cast<uint4*>(S.gvis);
+            const int n4 = (int)((A.gmask + 1) >> 1);  // gmask + 1 u64 words
+#pragma unroll 1
+            for (int i = lane; i < n4; i += 32) __stcg(t4 + i, make_uint4(0u, 0u, 0u, 0u));
+            __syncwarp();
+            S.epoch = 1u;
+        }
+    } else {
+        S.epoch = S.epoch == 0xFFFFFFFFu ? 1u : S.epoch + 1u;
+    }
     S.c_it = S.c_dc = S.c_tv = S.c_ne = S.c_dgs = S.c_ins = 0;
 
     // _initial_batch (search.py:207-227)

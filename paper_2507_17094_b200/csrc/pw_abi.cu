@@ -155,6 +155,7 @@ struct pw_shard {
     uint32_t* gepoch = nullptr;
     size_t gepoch_n = 0;
     int64_t gvis_stride = 0;  // per-warp table size the epochs are valid for
+    int gvis_lossy = 0;       // table holds lossy-cache words (else exact epoch entries)
     uint32_t* gscr = nullptr;
     size_t gscr_words = 0;
     std::mutex mu;
@@ -437,6 +438,18 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // the spill triggers when (smem entries + batch) > vis_limit, so a table is
     // needed whenever bound + CB can exceed it; it holds <= bound entries
     int64_t gsz = (specialised || bound + cb > A.vis_limit) ? next_pow2(2 * bound + 2) : 1;
+    // lossy visited cache (tuning flag 2): u32 (epoch8 << 24 | id) slots, so
+    // ids must fit 24 bits; never with log_visits (the log lists exact visits)
+    const bool lossy = tun && (tun->flags & 2) && std::max<int64_t>(sh->n, sh->gn) < (1 << 24) &&
+                       !p.log_visits;
+    A.lossy = lossy ? 1 : 0;
+    if (lossy) {
+        const int64_t slots = std::max<int64_t>(64, next_pow2(tun->visited_slots > 0 ? tun->visited_slots : 8192));
+        int lg = 0;
+        while ((1ll << lg) < slots) lg++;
+        A.lshift = 32 - lg;
+        gsz = slots / 2;  // u64 words of the per-warp region
+    }
     A.gmask = (int32_t)(gsz - 1);
     int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
     int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
@@ -462,13 +475,14 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         sh->gvis_words = words;
         sh->gepoch_n = (size_t)total_warps;
         sh->gvis_stride = gsz;
-    } else if (sh->gvis_stride != gsz) {
+    } else if (sh->gvis_stride != gsz || sh->gvis_lossy != (int)lossy) {
         // a different per-warp stride maps regions to other warps: re-zero so no
         // stale (epoch, id) of another warp can match
         PW_CUDA(cudaMemset(sh->gvis, 0, sizeof(unsigned long long) * sh->gvis_words));
         PW_CUDA(cudaMemset(sh->gepoch, 0, sizeof(uint32_t) * sh->gepoch_n));
         sh->gvis_stride = gsz;
     }
+    sh->gvis_lossy = (int)lossy;
     if (sh->gscr_words < (size_t)total_warps * scr) {
         if (sh->gscr) cudaFree(sh->gscr);
         sh->gscr = nullptr;

@@ -11,7 +11,7 @@ import pytest
 
 import oracle
 import paper_2507_17094_b200 as pw
-from golden_util import (GOLDEN, assert_run_equal, expected, load, oracle_dict, result_dict,
+from golden_util import (GOLDEN, assert_run_equal, assert_run_equal_lossy, expected, load, oracle_dict, result_dict,
                          sift_cases, small_cases)
 from paper_2507_17094_b200.rng import TAG_SEARCH, stream
 from paper_2507_17094_b200.search import SearchParams, ShardContext
@@ -261,3 +261,36 @@ def test_visited_spill_to_global_table(synth):
                                               tuning={"visited_slots": 256}))
     want = oracle_dict(oracle.run(queries, ctxs, params, "baseline"))
     assert_run_equal(got, want, "spill")
+
+
+LOSSY = {"flags": 2}
+
+
+@pytest.mark.parametrize("case", small_cases(), ids=lambda c: c[0])
+@pytest.mark.parametrize("slots", [8192, 64])
+def test_small_golden_lossy_visited(small, case, slots):
+    """Lossy visited cache: ids, distances and every counter but
+    distance_computations identical to the reference; 64 slots forces heavy
+    forgetting, so re-scored queued nodes must be dropped by the merge."""
+    name, params, mode, prefix = case
+    if params.log_visits:
+        pytest.skip("the visit log needs the exact set (lossy is ignored)")
+    z, base, queries, index, ctxs = small
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(queries, index, base, params, contexts=ctxs,
+                             tuning=dict(LOSSY, visited_slots=slots)))
+    assert_run_equal_lossy(got, expected(z, prefix), f"{name} lossy {slots}")
+
+
+@pytest.mark.parametrize("d", [96, 128, 200, 960])
+@pytest.mark.parametrize("arm", range(len(SYNTH_ARMS)))
+@pytest.mark.parametrize("mode", ["baseline", "pipelined"])
+@pytest.mark.parametrize("slots", [8192, 128])
+def test_synthetic_lossy_visited_matches_oracle(synth, d, arm, mode, slots):
+    queries, ctxs = synth[d]
+    params = SearchParams(**SYNTH_ARMS[arm])
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(pw.Dataset(queries), None, None, params, contexts=ctxs,
+                             tuning=dict(LOSSY, visited_slots=slots)))
+    want = oracle_dict(oracle.run(queries, ctxs, params, mode))
+    assert_run_equal_lossy(got, want, f"d={d} arm={arm} {mode} lossy {slots}")
