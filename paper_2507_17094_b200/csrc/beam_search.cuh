@@ -98,7 +98,7 @@ struct KArgs {
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
         o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
-    int32_t bulk_adj;       // adjacency / direction rows may use cp.async.bulk
+    int32_t bulk_adj;       // expansion rows 16-byte aligned: 1 cp.async x16, 2 TMA bulk (flag 4)
     int32_t prefetch;       // L2-prefetch predicted parent rows
     unsigned long long* phase;  // per-phase cycle totals (PW_PHASE_TIMERS builds only)
     int32_t vis_limit;      // smem visited entries before spilling to global
@@ -372,6 +372,26 @@ __device__ __forceinline__ float pw_leaf4(const float* x, const float* q, unsign
         for (int i = NF; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
         return s;
     }
+}
+
+// pw_leaf4 for a whole row of N <= 128 (N % 8 == 0) with this lane's query
+// pairs already in registers (qr[p] = q2[4p + c]): half the shared loads.
+template <int N>
+__device__ __forceinline__ float pw_row4_qreg(const float* x, const float2 (&qr)[N / 8], unsigned c) {
+    const float2* x2 = reinterpret_cast<const float2*>(x);
+    // packed FADD2/FMUL2 for (x - q)^2; the adds stay scalar: ptxas contracts
+    // mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (measured), which is not exact
+    float2 sq = sqd2(x2[c], qr[0]);
+    float r0 = sq.x, r1 = sq.y;
+#pragma unroll
+    for (int p = 1; p < N / 8; p++) {
+        sq = sqd2(x2[4 * p + c], qr[p]);
+        r0 = __fadd_rn(r0, sq.x);
+        r1 = __fadd_rn(r1, sq.y);
+    }
+    float a = __fadd_rn(r0, r1);
+    a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+    return __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
 }
 
 template <int OFF, int N>
@@ -769,6 +789,13 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
         issue(0);
         issue(1);
         const unsigned v = lane >> 2, c = lane & 3u;
+        constexpr bool QREG = D <= 128 && D % 8 == 0;
+        float2 qr[QREG ? D / 8 : 1];
+        if constexpr (QREG) {
+            const float2* q2 = reinterpret_cast<const float2*>(S.q);
+#pragma unroll
+            for (int p = 0; p < D / 8; p++) qr[p] = q2[4 * p + c];
+        }
         for (int g = 0; g < ngroups; g++) {
             cp_wait<1>();
             __syncwarp();
@@ -778,7 +805,11 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
             for (int pass = 0; pass < rows; pass += 8) {
                 const int rr = pass + (int)v;
                 const int rc = rr < rows ? rr : rows - 1;
-                const float dist = pw_sum4<0, D>(base + (size_t)rc * sp, S.q, c);
+                float dist;
+                if constexpr (QREG)
+                    dist = pw_row4_qreg<D>(base + (size_t)rc * sp, qr, c);
+                else
+                    dist = pw_sum4<0, D>(base + (size_t)rc * sp, S.q, c);
                 if (c == 0 && rr < rows) {
                     const uint32_t id = (uint32_t)S.newl[r0 + rr];
                     S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
@@ -1051,6 +1082,25 @@ static __device__ __noinline__ uint32_t bulk_issue_wait(const uint4* desc, uint6
     return phase ^ 4u;
 }
 
+// 16-byte aligned rows (the default): 8 lanes per row, 4 rows per warp step,
+// LDGSTS chunks.  TMA bulk copies need warp-uniform operands, so per-row
+// (data-dependent) sources make ptxas serialise lanes through a waterfall
+// loop of hundreds of instructions; this is a dozen.
+static __device__ __forceinline__ void copy16_issue_wait(const uint4* desc, int n_rows) {
+    const unsigned lane = lane_id();
+    const unsigned sub = lane & 7u;
+    for (int r = (int)(lane >> 3); r < n_rows; r += 4) {
+        const uint4 d = desc[r];
+        const char* src = reinterpret_cast<const char*>(((uint64_t)d.w << 32) | d.z);
+        const uint32_t nch = d.y >> 4;
+        for (uint32_t c = sub; c < nch; c += 8)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d.x + 16 * c), "l"(src + 16 * c));
+    }
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
+}
+
 // cp.async fallback for rows that are not 16-byte multiples (out of line).
 static __device__ __noinline__ void copy_issue_wait(const uint4* desc, int n_rows) {
     const unsigned lane = lane_id();
@@ -1091,8 +1141,10 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
         S.desc[r] = make_uint4(smem_u32(dst), bytes, (uint32_t)sp, (uint32_t)(sp >> 32));
     }
     __syncwarp();
-    if (A.bulk_adj)
+    if (A.bulk_adj == 2)
         S.phase = bulk_issue_wait(S.desc, S.mbar + 2, S.phase, n_rows, total);
+    else if (A.bulk_adj)
+        copy16_issue_wait(S.desc, n_rows);
     else
         copy_issue_wait(S.desc, n_rows);
 }
@@ -1294,6 +1346,16 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
     } while (0)
 #endif
 
+// log_visits (search.py:304-305): newly scored ids in batch order (cold).
+static __device__ __noinline__ int64_t log_visits(int32_t* log, int64_t cap, const int32_t* newl, int n_new,
+                                                  int64_t n_logged) {
+    for (int t = lane_id(); t < n_new; t += 32) {
+        const int64_t p = n_logged + t;
+        if (p < cap) log[p] = newl[t];
+    }
+    return n_logged + n_new;
+}
+
 // One full search (search.py:269-335) over graph G.  Seeds (already in
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
@@ -1372,13 +1434,8 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         int inserted = 0;
         if (A.prefetch && it > 0 && it < C.max_iter - 1) prefetch_parents<D>(A, S, G, C);
         if (n_new) {
-            if (C.log && A.visit_log) {
-                for (int t = lane; t < n_new; t += 32) {
-                    int64_t p = *n_logged + t;
-                    if (p < A.visit_cap) A.visit_log[task * A.visit_cap + p] = S.newl[t];
-                }
-                *n_logged += n_new;
-            }
+            if (C.log && A.visit_log)
+                *n_logged = log_visits(A.visit_log + task * A.visit_cap, A.visit_cap, S.newl, n_new, *n_logged);
             S.c_dc += n_new;
             PW_T(7);
             score_rows<D>(A, S, G, n_new);

@@ -412,7 +412,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.o_mbar = (int32_t)off;
     off = al(off + 3 * 8);
     A.o_desc = (int32_t)off;
-    off = al(off + 16 * 32);
+    off = al(off + 16 * std::max<int64_t>({32, (int64_t)p.r, 3ll * PG}));  // one descriptor per fetched row
     A.warp_bytes = (int32_t)off;
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
@@ -420,7 +420,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.prefetch = (tun && (tun->flags & 1)) ? 1 : 0;
     A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
                   (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16(4ll * d) && b16(4ll * G.j * W))))
-                     ? 1
+                     ? ((tun && (tun->flags & 4)) ? 2 : 1)
                      : 0;
 
     DevInfo* I;

@@ -65,3 +65,20 @@ def test_no_cpu_fallback_without_device():
                           global_ids=np.arange(4, dtype=np.int32))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         pw.search(np.zeros(2, np.float32), ctx, pw.SearchParams(k=1, l=4, m=4, r=1), rng=stream(0, 4, 0, 0))
+
+
+def test_no_fused_multiply_add_in_distance_code():
+    """Bit-exact L2 (numpy pairwise order, separately rounded sub/mul/add):
+    ptxas contracts packed mul.rn.f32x2 + add.rn.f32x2 into FFMA2, so the
+    kernels must contain no FFMA2 at all (and FMUL2 feeds scalar FADDs)."""
+    import shutil
+    import subprocess
+
+    from paper_2507_17094_b200 import _abi
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "beam_search_kernel" in sass
+    assert "FFMA2" not in sass
