@@ -638,28 +638,28 @@ static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint3
 // reference's.  A hit is never false: tags are unique per search and the
 // cache is cleared when the 8-bit epoch wraps.
 static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S, int nb) {
+    // all probes in flight at once as 4-byte LDGSTS into the (free until
+    // scoring) key area, then one compact pass: rolled loops, no register
+    // arrays (the hot loop has to stay within the instruction caches)
     const unsigned lane = lane_id();
     uint32_t* tab = reinterpret_cast<uint32_t*>(S.gvis);
+    uint32_t* vs = reinterpret_cast<uint32_t*>(S.ckey);
     const uint32_t tag = S.epoch << 24;
-    constexpr int K = 8;
+#pragma unroll 1
+    for (int t = lane; t < nb; t += 32) cp_async4(vs + t, tab + (hash32((uint32_t)S.newl[t]) >> A.lshift));
+    cp_commit();
+    cp_wait<0>();
+    __syncwarp();
     int cnt = 0;
-    for (int base0 = 0; base0 < nb; base0 += 32 * K) {
-        uint32_t id[K], v[K];
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            const int t = base0 + k * 32 + (int)lane;
-            id[k] = t < nb ? (uint32_t)S.newl[t] : 0u;
-            v[k] = t < nb ? __ldcg(&tab[hash32(id[k]) >> A.lshift]) : (tag | id[k]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int k = 0; k < K; k++) {
-            const bool fresh = v[k] != (tag | id[k]);
-            if (fresh) __stcg(&tab[hash32(id[k]) >> A.lshift], tag | id[k]);
-            const unsigned b = __ballot_sync(0xffffffffu, fresh);
-            if (fresh) S.newl[cnt + __popc(b & lanemask_lt())] = (int32_t)id[k];
-            cnt += __popc(b);
-        }
+#pragma unroll 1
+    for (int base = 0; base < nb; base += 32) {
+        const int t = base + (int)lane;
+        const uint32_t id = t < nb ? (uint32_t)S.newl[t] : 0u;
+        const bool fresh = t < nb && vs[t] != (tag | id);
+        if (fresh) __stcg(&tab[hash32(id) >> A.lshift], tag | id);
+        const unsigned b = __ballot_sync(0xffffffffu, fresh);
+        if (fresh) S.newl[cnt + __popc(b & lanemask_lt())] = (int32_t)id;
+        cnt += __popc(b);
     }
     __syncwarp();
     return cnt;
@@ -756,8 +756,9 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
 // reduced per warp pass in the compile-time pairwise order.  D == 0: generic
 // d (cp.async + runtime pairwise plan).
 template <int D>
-__device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n) {
+__device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n, uint64_t thr) {
     const unsigned lane = lane_id();
+    int ns = 0;  // survivors (key < thr, search.py:182-184) compacted into ckey as produced
     const int RH = A.R >> 1;
     const int sp = A.spad;
     const int ngroups = (n + RH - 1) / RH;
@@ -810,10 +811,11 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
                     dist = pw_row4_qreg<D>(base + (size_t)rc * sp, qr, c);
                 else
                     dist = pw_sum4<0, D>(base + (size_t)rc * sp, S.q, c);
-                if (c == 0 && rr < rows) {
-                    const uint32_t id = (uint32_t)S.newl[r0 + rr];
-                    S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
-                }
+                const uint64_t key = ((uint64_t)__float_as_uint(dist) << 32) | (uint32_t)S.newl[r0 + rc];
+                const bool surv = c == 0 && rr < rows && key < thr;
+                const unsigned b = __ballot_sync(0xffffffffu, surv);
+                if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
+                ns += __popc(b);
             }
             __syncwarp();
             issue(g + 2);
@@ -847,10 +849,11 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
                 int rr = sub + (int)v;
                 int rc = rr < rows ? rr : rows - 1;
                 float dist = l2_row(A.plan, base + (size_t)rc * sp, S.q, a);
-                if (a == 0 && rr < rows) {
-                    uint32_t id = (uint32_t)S.newl[r0 + rr];
-                    S.ckey[r0 + rr] = ((uint64_t)__float_as_uint(dist) << 32) | id;
-                }
+                const uint64_t key = ((uint64_t)__float_as_uint(dist) << 32) | (uint32_t)S.newl[r0 + rc];
+                const bool surv = a == 0 && rr < rows && key < thr;
+                const unsigned b = __ballot_sync(0xffffffffu, surv);
+                if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
+                ns += __popc(b);
             }
             __syncwarp();
             issue(g + 2);
@@ -858,6 +861,7 @@ __device__ void score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int 
         cp_wait<0>();
         __syncwarp();
     }
+    return ns;
 }
 
 // Bitonic sort of ckey[0..s) in shared memory (32 < s <= 256): compact
@@ -887,7 +891,7 @@ static __device__ __noinline__ void sort_survivors_smem(uint64_t* ckey, int s) {
 }
 
 // search.py:170-190 merge_and_sort on keys; returns `inserted`.
-static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int n) {
+static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg& C, int s) {
     // In place, single buffer: sort the survivors, find each one's insertion
     // point P_i = lower_bound(queue, S_i), shift only the queue tail
     // [min P_i, qlen) back to front (entry t moves to t + #{P_i <= t}; entries
@@ -898,18 +902,7 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     uint64_t* qk = S.qk0;
     uint8_t* qe = S.qe0;
     const int qlen = S.qlen;
-    const uint64_t thr = qlen == L ? qk[L - 1] : ~0ull;
-    int s = 0;  // survivors (compacted in place in ckey)
-    for (int base = 0; base < n; base += 32) {
-        int t = base + lane;
-        uint64_t key = t < n ? S.ckey[t] : ~0ull;
-        bool f = t < n && key < thr;
-        unsigned b = __ballot_sync(0xffffffffu, f);
-        int pos = s + __popc(b & lanemask_lt());
-        if (f) S.ckey[pos] = key;
-        s += __popc(b);
-    }
-    __syncwarp();
+    // ckey[0..s): the survivors (keys below the l-th key), filtered by score_rows
     if (s == 0) return 0;
     if (s <= 32) {
         uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
@@ -974,20 +967,20 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     S.fu = min(S.fu, pmin);  // entries before pmin keep their place (and flags)
     if (qlen > pmin) {
         // Queue tail [pmin, qlen): entry t moves to t + #{i : P_i <= t}.  Up to
-        // 8 chunks are read into registers, their targets found with
+        // 4 chunks are read into registers, their targets found with
         // independent bit-descent searches over ppos, then written -- back to
-        // front by 256-entry groups, so every write lands on an entry that was
+        // front by 128-entry groups, so every write lands on an entry that was
         // already read (targets are distinct and >= the source).
         int sstep = 1;
         while (sstep <= s) sstep <<= 1;
         sstep >>= 1;
-        for (int g_end = qlen; g_end > pmin; g_end -= 256) {
-            const int g0 = max(pmin, g_end - 256);
-            uint64_t key[8];
-            int np[8];
+        for (int g_end = qlen; g_end > pmin; g_end -= 128) {
+            const int g0 = max(pmin, g_end - 128);
+            uint64_t key[4];
+            int np[4];
             uint32_t fl = 0;
 #pragma unroll
-            for (int c = 0; c < 8; c++) {
+            for (int c = 0; c < 4; c++) {
                 const int t = g0 + 32 * c + (int)lane;
                 const bool valid = t < g_end;
                 key[c] = valid ? qk[t] : 0ull;
@@ -996,14 +989,14 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
             }
             for (int st = sstep; st > 0; st >>= 1) {
 #pragma unroll
-                for (int c = 0; c < 8; c++) {
+                for (int c = 0; c < 4; c++) {
                     const int t = g0 + 32 * c + (int)lane;
                     if (np[c] + st <= s && ppos[np[c] + st - 1] <= t) np[c] += st;
                 }
             }
             __syncwarp();
 #pragma unroll
-            for (int c = 0; c < 8; c++) {
+            for (int c = 0; c < 4; c++) {
                 const int t = g0 + 32 * c + (int)lane;
                 const int dst = t + np[c];
                 if (t < g_end && dst < L) {
@@ -1438,9 +1431,10 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
                 *n_logged = log_visits(A.visit_log + task * A.visit_cap, A.visit_cap, S.newl, n_new, *n_logged);
             S.c_dc += n_new;
             PW_T(7);
-            score_rows<D>(A, S, G, n_new);
+            const uint64_t thr = S.qlen == C.L ? S.qk0[C.L - 1] : ~0ull;
+            const int ns = score_rows<D>(A, S, G, n_new, thr);
             PW_T(1);
-            inserted = merge_queue(A, S, C, n_new);
+            inserted = merge_queue(A, S, C, ns);
             PW_T(2);
             S.c_ins += inserted;
         }
