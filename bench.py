@@ -50,6 +50,19 @@ CONFIGS = {
     "c2s": dict(workload="DEEP-shaped 1M x 96 f32 (C2 at 1/10 scale), 10K queries, k=10",
                 n=1_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
                 spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=32),
+    # BASELINE C3 / C5 are 100M points over 8 GPUs: one GPU holds one 12.5M
+    # shard, so the 1-GPU lines run exactly that shard's workload
+    "c3s": dict(workload="SIFT-shaped 12.5M x 128 uint8 (one of C3's 8 shards of 100M), 10K queries, "
+                         "k=10, degree-32 graph", n=12_500_000, d=128, nq=10_000, k=10, j=32,
+                gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=48,
+                dtype="u8"),
+    "c4": dict(workload="GIST-shaped 1M x 960 f32, 1K queries, k=10, degree-32 graph", n=1_000_000,
+               d=960, nq=1_000, k=10, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05,
+               rho=0.01, j_g=16, probe=48),
+    "c5s": dict(workload="Text2Image-shaped 12.5M x 200 f32 inner product (one of C5's 8 shards of "
+                         "100M), 10K queries, k=100, degree-32 graph", n=12_500_000, d=200, nq=10_000,
+                k=100, j=32, gen="latent", m=24, n_clusters=1, spread=1.0, noise=0.05, rho=0.01,
+                j_g=16, probe=48, metric="ip"),
     "tiny": dict(workload="smoke 20K x 96", n=20_000, d=96, nq=1_000, k=10, j=32, gen="latent",
                  m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=8),
 }
@@ -133,10 +146,18 @@ def build_workload(cfg: dict, rank: int, world: int, device):
     else:
         x = builder.gen_clustered(cfg["n"] + cfg["nq"], cfg["d"], cfg["n_clusters"],
                                   cfg["spread"], SEED, device=device)
+    if cfg.get("dtype") == "u8":
+        # SIFT-style bytes: the reference holds them as float32 (data.py:36);
+        # the shard keeps uint8 rows and the graph is built on the same values
+        x = torch.clamp(torch.round(128.0 + 40.0 * x), 0, 255)
+    if cfg.get("metric") == "ip":
+        # unit rows (embedding-style): the L2 kNN graph ranks like inner product
+        x = x / torch.linalg.vector_norm(x, dim=1, keepdim=True)
     base, queries = x[: cfg["n"]], x[cfg["n"]:].contiguous()
     parts = builder.partition(cfg["n"], world, SEED, device=device)
     rows = parts[rank]
     vec = base[rows].contiguous()
+    vec_dev = vec.to(torch.uint8) if cfg.get("dtype") == "u8" else vec
     adj = builder.knn_graph(vec, cfg["j"], probe=cfg["probe"], seed=SEED + rank)
     direction = builder.direction_table(vec, adj)
     gh = builder.ghost(vec, cfg["rho"], cfg["j_g"], SEED + rank)
@@ -147,24 +168,26 @@ def build_workload(cfg: dict, rank: int, world: int, device):
         del nxt
     torch.cuda.synchronize()
     build_s = time.time() - t0
-    return dict(base=base, queries=queries, rows=rows, vec=vec, adj=adj, direction=direction,
+    return dict(base=base, queries=queries, rows=rows, vec=vec_dev, adj=adj, direction=direction,
                 ghost=gh, inter=inter, build_s=build_s)
 
 
-def ground_truth(W: dict, k: int) -> np.ndarray:
+def ground_truth(W: dict, k: int, metric: str = "l2") -> np.ndarray:
     from paper_2507_17094_b200 import builder
 
+    if metric == "ip":
+        return builder.exact_mips_rescored(W["base"], W["queries"], k).cpu().numpy()
     return builder.exact_knn_rescored(W["base"], W["queries"], k).cpu().numpy()
 
 
-def arm_params(kind: str, l: int, k: int):
+def arm_params(kind: str, l: int, k: int, metric: str = "l2"):
     from paper_2507_17094_b200 import SearchParams
 
     if kind == "pathweaver":  # PPE + ghost staging + direction-guided selection
         return SearchParams(k=k, l=l, m=64, r=8, max_iter=64, seed=SEED % 1000,
                             selection="direction", discard_ratio=0.5, cooldown_ratio=0.3,
-                            ghost_enabled=True, ghost_max_iter=8)
-    return SearchParams(k=k, l=l, m=64, r=8, max_iter=64, seed=SEED % 1000)  # naive
+                            ghost_enabled=True, ghost_max_iter=8, metric=metric)
+    return SearchParams(k=k, l=l, m=64, r=8, max_iter=64, seed=SEED % 1000, metric=metric)  # naive
 
 
 # ------------------------------------------------------------------ arms
@@ -197,7 +220,8 @@ def run_ours(args, cfg):
                            W["inter"], gh_ids, gh_adj)
     log(f"[rank {rank}] index built in {W['build_s']:.1f}s; shard {shard.n} x {shard.d}, "
         f"{shard.nbytes / 1e9:.2f} GB on device")
-    truth = ground_truth(W, cfg["k"]) if rank == 0 else None
+    metric = cfg.get("metric", "l2")
+    truth = ground_truth(W, cfg["k"], metric) if rank == 0 else None
     queries = W["queries"]
     nq, k = queries.shape[0], cfg["k"]
     tuning = json.loads(args.tuning) if args.tuning else None
@@ -214,7 +238,7 @@ def run_ours(args, cfg):
         for l in L_GRID:
             if l < k:
                 continue
-            p = arm_params(kind, l, k)
+            p = arm_params(kind, l, k, metric)
             ids = search(p, mode)
             rec = builder.recall_at_k(ids, truth, k) if rank == 0 else 0.0
             if world > 1:
@@ -231,7 +255,7 @@ def run_ours(args, cfg):
         log(f"[rank {rank}] {kind}: sweep {sweep} -> l={chosen[0]}")
 
     def timed(kind, steps, warmup, with_timer=False):
-        p = arm_params(kind, ops[kind]["l"], k)
+        p = arm_params(kind, ops[kind]["l"], k, metric)
         mode = ops[kind]["mode"]
         for _ in range(warmup):
             search(p, mode)
@@ -270,7 +294,7 @@ def run_ours(args, cfg):
     # (tuning flag 2) the timed run re-scores a few forgotten nodes, so the
     # counters come from one exact-visited run (identical ids and counters
     # except distance_computations).
-    pw_params = arm_params("pathweaver", ops["pathweaver"]["l"], k)
+    pw_params = arm_params("pathweaver", ops["pathweaver"]["l"], k, metric)
     search(pw_params, "pipelined")
     dc_gathered = float(sum(s["distance_computations"].sum() for s in eng.last_stats())) / nq
     exact_tuning = dict(tuning or {})
@@ -280,6 +304,7 @@ def run_ours(args, cfg):
     stats = eng_exact.last_stats()
     seeded = set(range(1, world)) if world > 1 else set()
     bytes_step = dv.algorithmic_bytes(stats, pw_params, cfg["d"], cfg["j"], cfg["j_g"],
+                                      esize=1 if cfg.get("dtype") == "u8" else 4,
                                       seeded_stages=seeded)
     launches_per_step = max(1, launches // args.steps)
     peaks = {}
@@ -322,8 +347,10 @@ def run_ours(args, cfg):
             "metric": "QPS at recall@10=95%", "value": round(qps, 1), "unit": "queries/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.get("dtype", "f32"),
+            "data": "synthetic",
             "config": {"workload": cfg["workload"], "n": cfg["n"], "d": cfg["d"], "queries": nq,
+                       "metric": metric,
                        "k": k, "degree": cfg["j"], "shards": world,
                        "dist_backend": backend if world > 1 else None,
                        "arm": "pipelined path extension + ghost staging (rho=0.01) + direction-guided"
@@ -385,7 +412,7 @@ def host_index(W: dict):
     """Host copies of this rank's shard for the CPU oracle."""
     from paper_2507_17094_b200.search import GhostContext, ShardContext
 
-    vec = W["vec"].cpu().numpy()
+    vec = W["vec"].cpu().numpy().astype(np.float32, copy=False)  # u8 shards: the reference's upcast
     adj = W["adj"].cpu().numpy()
     ghost = None
     if W["ghost"] is not None:
@@ -440,7 +467,8 @@ def run_reference(args, cfg):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))) if torch.cuda.is_available() \
         else torch.device("cpu")
     W = build_workload(cfg, 0, 1, dev)  # index build is setup (GPU when present)
-    truth = ground_truth(W, cfg["k"])
+    metric = cfg.get("metric", "l2")
+    truth = ground_truth(W, cfg["k"], metric)
     ctx = host_index(W)
     qh = W["queries"].cpu().numpy()
     k = cfg["k"]
@@ -448,7 +476,7 @@ def run_reference(args, cfg):
     chosen = None
     sweep = []
     for l in L_GRID:
-        p = arm_params("pathweaver", l, k)
+        p = arm_params("pathweaver", l, k, metric)
         res = oracle.run(qh, [ctx], p, "pipelined", threads=threads)
         rec = builder.recall_at_k(res["final_ids"], truth, k)
         sweep.append((l, round(rec, 4)))
@@ -456,7 +484,7 @@ def run_reference(args, cfg):
             chosen = l
             break
     chosen = chosen or sweep[-1][0]
-    p = arm_params("pathweaver", chosen, k)
+    p = arm_params("pathweaver", chosen, k, metric)
     n = min(qh.shape[0], 2000)
     for _ in range(args.warmup):
         oracle.run(qh[:n], [ctx], p, "pipelined", threads=threads)
@@ -469,8 +497,9 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": "QPS at recall@10=95%", "value": round(qps, 1),
         "unit": "queries/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "l": chosen, "sweep": sweep, "shards": 1},
+        "scaling": "strong", "vs_baseline": None, "dtype": cfg.get("dtype", "f32"), "data": "synthetic",
+        "config": {"workload": cfg["workload"], "l": chosen, "sweep": sweep, "shards": 1,
+                   "metric": metric},
         "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{n} of {qh.shape[0]} queries per step (oracle/pw_oracle.c,"

@@ -24,6 +24,8 @@ extern "C" {
 #define PW_ENOMEM (-2)
 #define PW_ECUDA (-3)
 
+#define PW_METRIC_L2 0 /* squared L2, reported as sqrt (data.py:70-79, search.py:325) */
+#define PW_METRIC_IP 1 /* inner product: distance = -(q . x), pairwise-ordered; parity unpinned */
 #define PW_DTYPE_F32 0
 #define PW_DTYPE_U8 1
 
@@ -49,6 +51,7 @@ typedef struct {
     int32_t seed_mode;       /* PW_SEED_* */
     int32_t buffer_cap;      /* 0 = None */
     int32_t log_visits;
+    int32_t metric;          /* PW_METRIC_*: L2 (the reference's only metric) or IP (extension) */
 } pw_params;
 
 /* Device-side knobs outside SearchParams (SURVEY.md §5 "Config"). 0 = default. */
@@ -57,7 +60,10 @@ typedef struct {
     int32_t stage_rows;      /* rows in flight per warp (gather staging) */
     int32_t warps_per_sm;    /* cap on resident query-warps per SM */
     int32_t row_copy;        /* reserved (vector rows always use cp.async; TMA measured slower) */
-    int32_t flags;           /* bit 0: L2-prefetch predicted parent rows (off by default: measured slower) */
+    int32_t flags;           /* bit 0: L2-prefetch predicted parent rows (off by default: measured slower);
+                                bit 1: lossy visited cache (ids exact, distance_computations may grow);
+                                bit 2: TMA bulk copies for expansion rows; bit 3: L2 warm-up of scoring rows
+                                (bits 0, 2, 3 are measured slower; kept for A/B) */
 } pw_tuning;
 
 /* One shard (pipeline.py:121-155 build_contexts output for one ShardPack):

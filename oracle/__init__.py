@@ -53,6 +53,7 @@ class _Params(C.Structure):
         ("discard_ratio", C.c_double), ("cooldown_ratio", C.c_double),
         ("ghost_enabled", C.c_int32), ("ghost_max_iter", C.c_int32),
         ("seed_mode", C.c_int32), ("buffer_cap", C.c_int32), ("log_visits", C.c_int32),
+        ("metric", C.c_int32),
     ]
 
 
@@ -191,7 +192,8 @@ def _params(p) -> _Params:
     return _Params(int(p.k), int(p.l), int(p.m), int(p.r), int(p.max_iter),
                    int(p.seed) & (2**64 - 1), SELECTION[p.selection], float(p.discard_ratio),
                    float(p.cooldown_ratio), int(bool(p.ghost_enabled)), int(p.ghost_max_iter),
-                   SEED_MODE[p.seed_mode], int(p.buffer_cap or 0), int(bool(p.log_visits)))
+                   SEED_MODE[p.seed_mode], int(p.buffer_cap or 0), int(bool(p.log_visits)),
+                   {"l2": 0, "ip": 1}[getattr(p, "metric", "l2")])
 
 
 class _Keep:

@@ -290,6 +290,18 @@ static float sq_l2_row(const float* x, const float* q, int32_t d, float* tmp) {
     return pairwise_sum(tmp, d);
 }
 
+/* Inner-product distance (BASELINE C5; NOT in the reference -- parity
+ * unpinned, restated here so the device metric has a CPU checker):
+ * -(pairwise_sum(x * q)) with the same float32 pairwise order, no FMA. */
+static float neg_ip_row(const float* x, const float* q, int32_t d, float* tmp) {
+    for (int32_t t = 0; t < d; t++) tmp[t] = x[t] * q[t];
+    return -pairwise_sum(tmp, d);
+}
+
+static float metric_row(int32_t metric, const float* x, const float* q, int32_t d, float* tmp) {
+    return metric == 1 ? neg_ip_row(x, q, d, tmp) : sq_l2_row(x, q, d, tmp);
+}
+
 void orc_squared_l2(const float* points, int64_t rows, int32_t d, const float* q, float* out) {
     float* tmp = (float*)malloc(sizeof(float) * (size_t)(d > 0 ? d : 1));
     for (int64_t r = 0; r < rows; r++) out[r] = sq_l2_row(points + r * d, q, d, tmp);
@@ -481,7 +493,7 @@ int orc_search(const orc_graph* ctx, const float* query, const orc_params* p,
         for (int64_t b = 0; b < nb; b++) {
             int64_t v = batch[b];
             if (iset_has(&visited, v)) continue;
-            inc[n_new].d = sq_l2_row(ctx->vectors + v * d, query, d, tmp);
+            inc[n_new].d = metric_row(p->metric, ctx->vectors + v * d, query, d, tmp);
             inc[n_new].id = (int32_t)v;
             n_new++;
         }
@@ -562,7 +574,7 @@ int orc_search(const orc_graph* ctx, const float* query, const orc_params* p,
     for (int32_t t = 0; t < nk; t++) {
         out_local[t] = Q.q[t].id;
         out_ids[t] = ctx->global_ids[Q.q[t].id];
-        out_dists[t] = sqrtf(Q.q[t].d);
+        out_dists[t] = p->metric == 1 ? Q.q[t].d : sqrtf(Q.q[t].d);  /* search.py:325 (L2) */
     }
     res->n_out = nk;
     res->converged = converged;

@@ -51,6 +51,7 @@ typedef struct {
     int32_t seed_mode;        /* 0 neighbors, 1 mixed */
     int32_t buffer_cap;       /* 0 = None */
     int32_t log_visits;
+    int32_t metric;           /* 0 L2 (the reference); 1 inner product (extension, parity unpinned) */
 } orc_params;
 
 /* numpy PCG64 bit generator state (128-bit state/inc + buffered uint32). */

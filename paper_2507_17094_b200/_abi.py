@@ -25,7 +25,7 @@ class Params(C.Structure):
         ("max_iter", C.c_int32), ("seed", C.c_uint64), ("selection", C.c_int32),
         ("discard_ratio", C.c_double), ("cooldown_ratio", C.c_double),
         ("ghost_enabled", C.c_int32), ("ghost_max_iter", C.c_int32), ("seed_mode", C.c_int32),
-        ("buffer_cap", C.c_int32), ("log_visits", C.c_int32),
+        ("buffer_cap", C.c_int32), ("log_visits", C.c_int32), ("metric", C.c_int32),
     ]
 
 
@@ -133,7 +133,11 @@ def params_struct(p) -> Params:
     return Params(int(p.k), int(p.l), int(p.m), int(p.r), int(p.max_iter),
                   int(p.seed) & (2**64 - 1), SELECTION[p.selection], float(p.discard_ratio),
                   float(p.cooldown_ratio), int(bool(p.ghost_enabled)), int(p.ghost_max_iter),
-                  SEED_MODE[p.seed_mode], int(p.buffer_cap or 0), int(bool(p.log_visits)))
+                  SEED_MODE[p.seed_mode], int(p.buffer_cap or 0), int(bool(p.log_visits)),
+                  METRIC[getattr(p, "metric", "l2")])
+
+
+METRIC = {"l2": 0, "ip": 1}
 
 
 def tuning_struct(t) -> Tuning:

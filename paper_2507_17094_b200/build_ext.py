@@ -21,8 +21,10 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = PKG / "_build"
 OUT = PKG / "libpwb200.so"
-# must match PW_DIMS in csrc/pw_abi.cu (0 = generic d)
+# must match PW_DIMS / PW_DIMS_U8 / PW_DIMS_IP in csrc/pw_abi.cu (0 = generic d)
 DIMS = (0, 16, 32, 64, 96, 100, 128, 200, 256, 384, 512, 768, 960, 1024)
+DIMS_U8 = (0, 96, 128)
+DIMS_IP = (0, 96, 128, 200)
 DEPS = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "pw_b200.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -68,6 +70,14 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
         obj = bdir / f"k_{d}.o"
         jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",
                            str(obj)], obj))
+    for d in DIMS_U8:
+        obj = bdir / f"k_u8_{d}.o"
+        jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-DPW_U8", "-c", str(CSRC / "k_inst.cu"),
+                           "-o", str(obj)], obj))
+    for d in DIMS_IP:
+        obj = bdir / f"k_ip_{d}.o"
+        jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-DPW_IP", "-c", str(CSRC / "k_inst.cu"),
+                           "-o", str(obj)], obj))
     workers = jobs or max(1, min(len(jobs_list), os.cpu_count() or 1))
     with ThreadPoolExecutor(workers) as pool:
         logs = list(pool.map(lambda j: _run(j[0]), jobs_list))

@@ -329,6 +329,43 @@ def exact_knn_rescored(base: torch.Tensor, queries: torch.Tensor, k: int, pad: i
     return out
 
 
+def exact_mips_rescored(base: torch.Tensor, queries: torch.Tensor, k: int, pad: int = 8,
+                        qchunk: int = 1024, bchunk: int = 1 << 21) -> torch.Tensor:
+    """Inner-product ground truth (BASELINE C5): fp32 GEMM screen for the
+    k+pad largest q.x, float64 rescore, rank by (-q.x, id)."""
+    dev = base.device
+    nq = queries.shape[0]
+    kk = k + pad
+    out = torch.empty((nq, k), dtype=torch.int64, device=dev)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        for qlo in range(0, nq, qchunk):
+            qhi = min(nq, qlo + qchunk)
+            best_v = best_i = None
+            for blo in range(0, base.shape[0], bchunk):
+                bhi = min(base.shape[0], blo + bchunk)
+                s = queries[qlo:qhi] @ base[blo:bhi].T
+                t = torch.topk(s, min(kk, bhi - blo), dim=1, largest=True)
+                v, i = t.values, t.indices + blo
+                if best_v is not None:
+                    v = torch.cat([best_v, v], 1)
+                    i = torch.cat([best_i, i], 1)
+                    t2 = torch.topk(v, min(kk, v.shape[1]), dim=1, largest=True)
+                    v, i = t2.values, torch.gather(i, 1, t2.indices)
+                best_v, best_i = v, i
+            c = best_i
+            sc = (base[c].double() * queries[qlo:qhi, None, :].double()).sum(2)
+            order = torch.argsort(c, 1)
+            c2 = torch.gather(c, 1, order)
+            s2 = torch.gather(-sc, 1, order)
+            o2 = torch.sort(s2, dim=1, stable=True).indices
+            out[qlo:qhi] = torch.gather(c2, 1, o2)[:, :k]
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return out
+
+
 def direction_table(x: torch.Tensor, adj: torch.Tensor, chunk: int = 1 << 16) -> torch.Tensor:
     """graphs.py:177-186: bit t of word t//32 = x[nbr][t] >= x[node][t]."""
     n, j = adj.shape

@@ -30,7 +30,7 @@ constexpr int kMaxOps = 2 * kMaxLeaves;
 constexpr int kParentGroup = 8;
 
 struct GraphDev {
-    const float* vec;       // (n, d) f32 rows
+    const void* vec;        // (n, d) rows of the shard's element type (f32 or u8)
     const int32_t* adj;     // (n, j)
     const int32_t* gid;     // (n,) output id map
     const uint32_t* dir;    // (n, j, W) or null
@@ -65,7 +65,7 @@ struct KArgs {
     GraphDev main, ghost;
     const int32_t* inter;   // (n,) or null
     int32_t d, W;
-    int32_t spad;           // staging row stride in floats (== 8 mod 32)
+    int32_t spad;           // staging row stride in elements (bank-conflict-free passes)
     L2Plan plan;
     SearchCfg cfg, gcfg;
     int32_t ghost_on;       // run the ghost prologue when the task has no entry
@@ -93,13 +93,14 @@ struct KArgs {
     int64_t visit_cap;
     // per-warp shared-memory layout (bytes)
     int32_t L_max, CB, BH, H, R, PG;
-    int32_t pstride;        // DGS parent-row stride in floats (16-byte multiple)
+    int32_t pstride;        // DGS parent-row stride in elements (16-byte multiple)
     int32_t o_par;          // parents list offset in misc (words)
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
         o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
     int32_t bulk_adj;       // expansion rows 16-byte aligned: 1 cp.async x16, 2 TMA bulk (flag 4)
     int32_t prefetch;       // L2-prefetch predicted parent rows
+    int32_t warm_rows;      // L2-prefetch every row of a scoring batch beyond the first two groups
     unsigned long long* phase;  // per-phase cycle totals (PW_PHASE_TIMERS builds only)
     int32_t vis_limit;      // smem visited entries before spilling to global
     unsigned long long* gvis;  // per-warp global visited spill tables, (epoch << 32 | id)
@@ -253,6 +254,20 @@ __device__ __forceinline__ void warp_copy_async(void* dst, const void* src, int 
     }
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Vector element types: float32 rows, or uint8 rows (SIFT-style bvecs) that
+// the reference upcasts to float32 (data.py:36) -- float(b) is exact, so the
+// arithmetic after the load is identical.
+template <typename VT>
+__device__ __forceinline__ const VT* vrow(const GraphDev& G, uint32_t id, int d) {
+    return reinterpret_cast<const VT*>(G.vec) + (size_t)id * d;
+}
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(uint8_t x) { return (float)x; }
+
 __device__ __forceinline__ float sqd(float x, float q) {
     float df = __fsub_rn(x, q);
     return __fmul_rn(df, df);
@@ -269,87 +284,94 @@ __device__ __forceinline__ float2 sqd2(float2 x, float2 q) {
     return *reinterpret_cast<const float2*>(&r);
 }
 
+// Metric element op, summed in the numpy pairwise order: M = 0 squared L2
+// (data.py:70-79, the reference's only metric); M = 1 inner product
+// (BASELINE C5, an extension -- parity unpinned): x*q, and the distance is
+// the negated sum so that smaller is better everywhere.
+template <int M>
+__device__ __forceinline__ float eop(float x, float q) {
+    if constexpr (M == 0) return sqd(x, q);
+    else return __fmul_rn(x, q);
+}
+template <int M>
+__device__ __forceinline__ float2 eop2(float2 x, float2 q) {
+    if constexpr (M == 0) {
+        return sqd2(x, q);
+    } else {
+        unsigned long long xv = *reinterpret_cast<const unsigned long long*>(&x);
+        unsigned long long qv = *reinterpret_cast<const unsigned long long*>(&q);
+        unsigned long long r;
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(xv), "l"(qv));
+        return *reinterpret_cast<const float2*>(&r);
+    }
+}
+template <int M>
+__device__ __forceinline__ float finish(float sum) { return M == 0 ? sum : -sum; }
+// Queue keys: distance bits << 32 | id.  L2 distances are >= 0, so raw bits
+// order like the floats; IP distances can be negative: sign-flip transform.
+template <int M>
+__device__ __forceinline__ uint32_t dist_bits(float d) {
+    uint32_t b = __float_as_uint(d);
+    if constexpr (M == 0) {
+        return b;
+    } else {
+        if (b == 0x80000000u) b = 0u;  // -0 == +0 as floats (the oracle compares floats)
+        return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    }
+}
+template <int M>
+__device__ __forceinline__ float bits_dist(uint32_t k) {
+    if constexpr (M == 0) return __uint_as_float(k);
+    else return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+
 // numpy pairwise_sum leaf over squared differences, lanes (v, a=lane&7)
 // hold accumulator a; every lane of the 8-lane group ends with the leaf sum.
-__device__ __forceinline__ float l2_leaf(const float* x, const float* q, int off, int len,
-                                         unsigned a) {
+template <int M, typename VT>
+__device__ __forceinline__ float l2_leaf(const VT* x, const float* q, int off, int len, unsigned a) {
     if (len < 8) {
         float s = 0.f;
-        for (int i = 0; i < len; i++) s = __fadd_rn(s, sqd(x[off + i], q[off + i]));
+        for (int i = 0; i < len; i++) s = __fadd_rn(s, eop<M>(to_f(x[off + i]), q[off + i]));
         return s;
     }
     const int nf = len - (len & 7);
-    float acc = sqd(x[off + a], q[off + a]);
-    for (int i = off + (int)a + 8; i < off + nf; i += 8) acc = __fadd_rn(acc, sqd(x[i], q[i]));
+    float acc = eop<M>(to_f(x[off + a]), q[off + a]);
+    for (int i = off + (int)a + 8; i < off + nf; i += 8) acc = __fadd_rn(acc, eop<M>(to_f(x[i]), q[i]));
     acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 1));
     acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 2));
     acc = __fadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, 4));
-    for (int i = off + nf; i < off + len; i++) acc = __fadd_rn(acc, sqd(x[i], q[i]));
+    for (int i = off + nf; i < off + len; i++) acc = __fadd_rn(acc, eop<M>(to_f(x[i]), q[i]));
     return acc;
 }
 
-__device__ __forceinline__ float l2_row(const L2Plan& P, const float* x, const float* q,
-                                        unsigned a) {
-    if (P.n_leaves == 1) return l2_leaf(x, q, 0, P.leaf_len[0], a);
+// Pairwise-ordered sum over a row (runtime plan), metric-finished.
+template <int M, typename VT>
+__device__ __forceinline__ float l2_row(const L2Plan& P, const VT* x, const float* q, unsigned a) {
+    if (P.n_leaves == 1) return finish<M>(l2_leaf<M>(x, q, 0, P.leaf_len[0], a));
     float stack[8];
     int sp = 0;
     for (int o = 0; o < P.n_ops; o++) {
         int op = P.ops[o];
         if (op >= 0) {
-            stack[sp++] = l2_leaf(x, q, P.leaf_off[op], P.leaf_len[op], a);
+            stack[sp++] = l2_leaf<M>(x, q, P.leaf_off[op], P.leaf_len[op], a);
         } else {
             float b = stack[--sp];
             float t = stack[--sp];
             stack[sp++] = __fadd_rn(t, b);
         }
     }
-    return stack[0];
-}
-
-// Compile-time numpy pairwise order for row length N at offset OFF, lane
-// layout (row v = lane>>1, half h = lane&1): half h owns accumulators
-// 4h..4h+3 and reads them as one float4 per 8-element step.
-template <int OFF, int N>
-__device__ __forceinline__ float pw_leaf(const float* x, const float* q, unsigned h) {
-    if constexpr (N < 8) {
-        float s = 0.f;
-#pragma unroll
-        for (int i = 0; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
-        return s;
-    } else {
-        constexpr int NF = N - (N % 8);
-        const float4* x4 = reinterpret_cast<const float4*>(x + OFF);
-        const float4* q4 = reinterpret_cast<const float4*>(q + OFF);
-        float4 xv = x4[h], qv = q4[h];
-        float r0 = sqd(xv.x, qv.x), r1 = sqd(xv.y, qv.y), r2 = sqd(xv.z, qv.z), r3 = sqd(xv.w, qv.w);
-#pragma unroll
-        for (int p = 1; p < NF / 8; p++) {
-            xv = x4[2 * p + h];
-            qv = q4[2 * p + h];
-            r0 = __fadd_rn(r0, sqd(xv.x, qv.x));
-            r1 = __fadd_rn(r1, sqd(xv.y, qv.y));
-            r2 = __fadd_rn(r2, sqd(xv.z, qv.z));
-            r3 = __fadd_rn(r3, sqd(xv.w, qv.w));
-        }
-        // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)): IEEE add is commutative, so
-        // both halves end with the bit-identical value
-        float a = __fadd_rn(__fadd_rn(r0, r1), __fadd_rn(r2, r3));
-        float s = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
-#pragma unroll
-        for (int i = NF; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
-        return s;
-    }
+    return finish<M>(stack[0]);
 }
 
 // Same order with 4 lanes per row (8 rows per warp pass): lane c = lane&3
 // owns accumulators 2c, 2c+1 (one float2 per 8-element step); the xor-1 and
 // xor-2 shuffles form ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)).
-template <int OFF, int N>
+template <int M, int OFF, int N>
 __device__ __forceinline__ float pw_leaf4(const float* x, const float* q, unsigned c) {
     if constexpr (N < 8) {
         float s = 0.f;
 #pragma unroll
-        for (int i = 0; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
+        for (int i = 0; i < N; i++) s = __fadd_rn(s, eop<M>(x[OFF + i], q[OFF + i]));
         return s;
     } else {
         constexpr int NF = N - (N % 8);
@@ -357,11 +379,11 @@ __device__ __forceinline__ float pw_leaf4(const float* x, const float* q, unsign
         const float2* q2 = reinterpret_cast<const float2*>(q + OFF);
         // packed FADD2/FMUL2 for (x - q)^2 on both accumulators; the adds stay
         // scalar so ptxas cannot contract mul+add into FFMA2 (bit-exactness)
-        float2 sq = sqd2(x2[c], q2[c]);
+        float2 sq = eop2<M>(x2[c], q2[c]);
         float r0 = sq.x, r1 = sq.y;
 #pragma unroll
         for (int p = 1; p < NF / 8; p++) {
-            sq = sqd2(x2[4 * p + c], q2[4 * p + c]);
+            sq = eop2<M>(x2[4 * p + c], q2[4 * p + c]);
             r0 = __fadd_rn(r0, sq.x);
             r1 = __fadd_rn(r1, sq.y);
         }
@@ -369,54 +391,73 @@ __device__ __forceinline__ float pw_leaf4(const float* x, const float* q, unsign
         a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
         float s = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
 #pragma unroll
-        for (int i = NF; i < N; i++) s = __fadd_rn(s, sqd(x[OFF + i], q[OFF + i]));
+        for (int i = NF; i < N; i++) s = __fadd_rn(s, eop<M>(x[OFF + i], q[OFF + i]));
         return s;
     }
 }
 
 // pw_leaf4 for a whole row of N <= 128 (N % 8 == 0) with this lane's query
 // pairs already in registers (qr[p] = q2[4p + c]): half the shared loads.
-template <int N>
+template <int M, int N>
 __device__ __forceinline__ float pw_row4_qreg(const float* x, const float2 (&qr)[N / 8], unsigned c) {
     const float2* x2 = reinterpret_cast<const float2*>(x);
     // packed FADD2/FMUL2 for (x - q)^2; the adds stay scalar: ptxas contracts
     // mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (measured), which is not exact
-    float2 sq = sqd2(x2[c], qr[0]);
+    float2 sq = eop2<M>(x2[c], qr[0]);
     float r0 = sq.x, r1 = sq.y;
 #pragma unroll
     for (int p = 1; p < N / 8; p++) {
-        sq = sqd2(x2[4 * p + c], qr[p]);
+        sq = eop2<M>(x2[4 * p + c], qr[p]);
         r0 = __fadd_rn(r0, sq.x);
         r1 = __fadd_rn(r1, sq.y);
     }
     float a = __fadd_rn(r0, r1);
     a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
-    return __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2));
+    return finish<M>(__fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2)));
 }
 
-template <int OFF, int N>
+// Same for uint8 rows: lane c reads its two bytes of every 8-byte step
+// (LDS.U16), rebuilds float(b) exactly as (2^23 + b) - 2^23 (PRMT + FADD2,
+// full-rate ALUs instead of I2F), then the float32 ops of pw_row4_qreg.
+template <int M, int N>
+__device__ __forceinline__ float pw_row4_u8(const uint8_t* x, const float2 (&qr)[N / 8], unsigned c) {
+    const uint16_t* x2 = reinterpret_cast<const uint16_t*>(x);
+    const float2 big = make_float2(8388608.f, 8388608.f);
+    auto ld = [&](int p) -> float2 {
+        const uint32_t w = x2[4 * p + c];
+        const float2 f = make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540)),
+                                     __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7541)));
+        unsigned long long fv = *reinterpret_cast<const unsigned long long*>(&f);
+        unsigned long long bv = *reinterpret_cast<const unsigned long long*>(&big);
+        unsigned long long r;
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(fv), "l"(bv));
+        return *reinterpret_cast<const float2*>(&r);
+    };
+    float2 sq = eop2<M>(ld(0), qr[0]);
+    float r0 = sq.x, r1 = sq.y;
+#pragma unroll
+    for (int p = 1; p < N / 8; p++) {
+        sq = eop2<M>(ld(p), qr[p]);
+        r0 = __fadd_rn(r0, sq.x);
+        r1 = __fadd_rn(r1, sq.y);
+    }
+    float a = __fadd_rn(r0, r1);
+    a = __fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 1));
+    return finish<M>(__fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2)));
+}
+
+template <int M, int OFF, int N>
 __device__ __forceinline__ float pw_sum4(const float* x, const float* q, unsigned c) {
     if constexpr (N <= 128) {
-        return pw_leaf4<OFF, N>(x, q, c);
+        return pw_leaf4<M, OFF, N>(x, q, c);
     } else {
         constexpr int N2 = N / 2 - (N / 2) % 8;
-        float a = pw_sum4<OFF, N2>(x, q, c);
-        float b = pw_sum4<OFF + N2, N - N2>(x, q, c);
+        float a = pw_sum4<M, OFF, N2>(x, q, c);
+        float b = pw_sum4<M, OFF + N2, N - N2>(x, q, c);
         return __fadd_rn(a, b);
     }
 }
 
-template <int OFF, int N>
-__device__ __forceinline__ float pw_sum(const float* x, const float* q, unsigned h) {
-    if constexpr (N <= 128) {
-        return pw_leaf<OFF, N>(x, q, h);
-    } else {
-        constexpr int N2 = N / 2 - (N / 2) % 8;
-        float a = pw_sum<OFF, N2>(x, q, h);
-        float b = pw_sum<OFF + N2, N - N2>(x, q, h);
-        return __fadd_rn(a, b);
-    }
-}
 
 // --------------------------------------------------------------- per warp
 struct WarpState {
@@ -755,7 +796,7 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
 // completion on a per-half mbarrier, two halves in flight), and 16 rows are
 // reduced per warp pass in the compile-time pairwise order.  D == 0: generic
 // d (cp.async + runtime pairwise plan).
-template <int D>
+template <int D, typename VT, int M>
 __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n, uint64_t thr) {
     const unsigned lane = lane_id();
     int ns = 0;  // survivors (key < thr, search.py:182-184) compacted into ckey as produced
@@ -763,34 +804,52 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
     const int sp = A.spad;
     const int ngroups = (n + RH - 1) / RH;
     if constexpr (D > 0) {
-        constexpr uint32_t row_bytes = D * 4;
-        constexpr int CPR = D / 4;  // 16-byte chunks per row
+        constexpr uint32_t row_bytes = D * (uint32_t)sizeof(VT);
+        constexpr int CPR = row_bytes / 16;  // 16-byte chunks per row
         auto issue = [&](int g) {
             if (g < ngroups) {
                 const int r0 = g * RH;
                 const int rows = min(RH, n - r0);
-                float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
+                VT* dst0 = reinterpret_cast<VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
                 // LDGSTS: LPR lanes per row, CPL 16-byte chunks per lane
                 constexpr int LPR = CPR <= 32 ? 8 : 32;
                 constexpr int CPL = (CPR + LPR - 1) / LPR;
                 constexpr int RPP = 32 / LPR;
                 const int sub = (int)lane % LPR;
                 for (int r = (int)lane / LPR; r < rows; r += RPP) {
-                    const float* src = G.vec + (size_t)S.newl[r0 + r] * D;
-                    float* dst = dst0 + (size_t)r * sp;
+                    const VT* src = vrow<VT>(G, (uint32_t)S.newl[r0 + r], D);
+                    VT* dst = dst0 + (size_t)r * sp;
 #pragma unroll
                     for (int k = 0; k < CPL; k++) {
                         const int ch = sub + k * LPR;
-                        if (CPR % LPR == 0 || ch < CPR) cp_async16(dst + 4 * ch, src + 4 * ch);
+                        if (CPR % LPR == 0 || ch < CPR) cp_async16(dst + (16 / sizeof(VT)) * ch, src + (16 / sizeof(VT)) * ch);
                     }
                 }
             }
             cp_commit();
         };
+        // L2 warm-up two groups ahead of the staging ring (prefetch.global.L2,
+        // no staging space): group g+4 is requested while g is reduced, so its
+        // LDGSTS two steps later hits L2.  A bounded window: warming the whole
+        // batch at once overflows L2 across ~2400 resident queries (measured).
+        constexpr int LINES = (row_bytes % 128 == 0) ? row_bytes / 128 : row_bytes / 128 + 2;
+        auto warm = [&](int g) {
+            if (A.warm_rows && g < ngroups) {
+                const int r0 = g * RH;
+                const int rows = min(RH, n - r0);
+                for (int i = (int)lane; i < rows * LINES; i += 32) {
+                    const int r = i / LINES, k = i - r * LINES;
+                    const char* row = reinterpret_cast<const char*>(vrow<VT>(G, (uint32_t)S.newl[r0 + r], D));
+                    prefetch_l2(row + min(k * 128, (int)row_bytes - 4));
+                }
+            }
+        };
         issue(0);
         issue(1);
+        warm(2);
+        warm(3);
         const unsigned v = lane >> 2, c = lane & 3u;
-        constexpr bool QREG = D <= 128 && D % 8 == 0;
+        constexpr bool QREG = (D <= 128 && D % 8 == 0) || sizeof(VT) == 1;
         float2 qr[QREG ? D / 8 : 1];
         if constexpr (QREG) {
             const float2* q2 = reinterpret_cast<const float2*>(S.q);
@@ -802,16 +861,18 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             __syncwarp();
             const int r0 = g * RH;
             const int rows = min(RH, n - r0);
-            const float* base = S.stage + (size_t)(g & 1) * RH * sp;
+            const VT* base = reinterpret_cast<const VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
             for (int pass = 0; pass < rows; pass += 8) {
                 const int rr = pass + (int)v;
                 const int rc = rr < rows ? rr : rows - 1;
                 float dist;
-                if constexpr (QREG)
-                    dist = pw_row4_qreg<D>(base + (size_t)rc * sp, qr, c);
+                if constexpr (sizeof(VT) == 1)
+                    dist = pw_row4_u8<M, D>(reinterpret_cast<const uint8_t*>(base + (size_t)rc * sp), qr, c);
+                else if constexpr (QREG)
+                    dist = pw_row4_qreg<M, D>(reinterpret_cast<const float*>(base + (size_t)rc * sp), qr, c);
                 else
-                    dist = pw_sum4<0, D>(base + (size_t)rc * sp, S.q, c);
-                const uint64_t key = ((uint64_t)__float_as_uint(dist) << 32) | (uint32_t)S.newl[r0 + rc];
+                    dist = finish<M>(pw_sum4<M, 0, D>(reinterpret_cast<const float*>(base + (size_t)rc * sp), S.q, c));
+                const uint64_t key = ((uint64_t)dist_bits<M>(dist) << 32) | (uint32_t)S.newl[r0 + rc];
                 const bool surv = c == 0 && rr < rows && key < thr;
                 const unsigned b = __ballot_sync(0xffffffffu, surv);
                 if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
@@ -819,19 +880,20 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             }
             __syncwarp();
             issue(g + 2);
+            warm(g + 4);
         }
         cp_wait<0>();
         __syncwarp();
     } else {
-        const int row_bytes = A.d * 4;
+        const int row_bytes = A.d * (int)sizeof(VT);
         auto issue = [&](int g) {
             if (g < ngroups) {
                 int r0 = g * RH;
                 int rows = min(RH, n - r0);
-                float* dst0 = S.stage + (size_t)(g & 1) * RH * sp;
+                VT* dst0 = reinterpret_cast<VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
                 for (int r = 0; r < rows; r++) {
                     int32_t id = S.newl[r0 + r];
-                    warp_copy_async(dst0 + (size_t)r * sp, G.vec + (size_t)id * A.d, row_bytes);
+                    warp_copy_async(dst0 + (size_t)r * sp, vrow<VT>(G, (uint32_t)id, A.d), row_bytes);
                 }
             }
             cp_commit();
@@ -844,12 +906,12 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             __syncwarp();
             int r0 = g * RH;
             int rows = min(RH, n - r0);
-            const float* base = S.stage + (size_t)(g & 1) * RH * sp;
+            const VT* base = reinterpret_cast<const VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
             for (int sub = 0; sub < rows; sub += 4) {
                 int rr = sub + (int)v;
                 int rc = rr < rows ? rr : rows - 1;
-                float dist = l2_row(A.plan, base + (size_t)rc * sp, S.q, a);
-                const uint64_t key = ((uint64_t)__float_as_uint(dist) << 32) | (uint32_t)S.newl[r0 + rc];
+                float dist = l2_row<M>(A.plan, base + (size_t)rc * sp, S.q, a);
+                const uint64_t key = ((uint64_t)dist_bits<M>(dist) << 32) | (uint32_t)S.newl[r0 + rc];
                 const bool surv = a == 0 && rr < rows && key < thr;
                 const unsigned b = __ballot_sync(0xffffffffu, surv);
                 if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
@@ -1142,15 +1204,12 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
         copy_issue_wait(S.desc, n_rows);
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
 // Warm L2 with the rows the next expansion will most likely fetch: the first
 // r unexpanded entries of the current queue become the parents unless new
 // candidates overtake them.  One prefetch per 128-byte line, no registers
 // tied up; a wrong guess only costs bandwidth.
-template <int D>
+template <int D, typename VT>
 __device__ __forceinline__ void prefetch_parents(const KArgs& A, const WarpState& S, const GraphDev& G,
                                                  const SearchCfg& C) {
     const unsigned lane = lane_id();
@@ -1167,8 +1226,8 @@ __device__ __forceinline__ void prefetch_parents(const KArgs& A, const WarpState
     for (int o = 0; o < j * 4; o += 128) prefetch_l2(a + o);
     if (C.prune_sel == 1 && G.dir) {
         const int d = D > 0 ? D : A.d;
-        const char* v = reinterpret_cast<const char*>(G.vec + (size_t)par * d);
-        for (int o = 0; o < d * 4; o += 128) prefetch_l2(v + o);
+        const char* v = reinterpret_cast<const char*>(vrow<VT>(G, par, d));
+        for (int o = 0; o < d * (int)sizeof(VT); o += 128) prefetch_l2(v + o);
         const char* dr = reinterpret_cast<const char*>(G.dir + (size_t)par * j * A.W);
         for (int o = 0; o < j * A.W * 4; o += 128) prefetch_l2(dr + o);
     }
@@ -1176,7 +1235,7 @@ __device__ __forceinline__ void prefetch_parents(const KArgs& A, const WarpState
 
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
 // returns the candidate count p * n_sel.
-template <int D>
+template <int D, typename VT>
 __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                       const int32_t* parents, int np, int it, Pcg64& rng) {
     const unsigned lane = lane_id();
@@ -1201,11 +1260,11 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
         constexpr int WC = D > 0 ? (D + 31) / 32 : 0;
         const int W = WC ? WC : A.W;
         const int d = D > 0 ? D : A.d;
-        const uint32_t vec_bytes = (uint32_t)d * 4u, dir_bytes = (uint32_t)(j * W) * 4u;
+        const uint32_t vec_bytes = (uint32_t)d * (uint32_t)sizeof(VT), dir_bytes = (uint32_t)(j * W) * 4u;
         for (int pg = 0; pg < np; pg += A.PG) {
             const int gp = min(A.PG, np - pg);
-            float* prow = S.stage;
-            uint32_t* drow = reinterpret_cast<uint32_t*>(S.stage + (size_t)gp * A.pstride);
+            VT* prow = reinterpret_cast<VT*>(S.stage);
+            uint32_t* drow = reinterpret_cast<uint32_t*>(prow + (size_t)gp * A.pstride);
             fetch_group(A, S, 3 * gp, gp * (adj_bytes + vec_bytes + dir_bytes),
                         [&](int r, void*& dst, const void*& src, uint32_t& b) {
                             const int pi = r % gp, kind = r / gp;
@@ -1216,7 +1275,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                                 b = adj_bytes;
                             } else if (kind == 1) {
                                 dst = prow + (size_t)pi * A.pstride;
-                                src = G.vec + (size_t)par * d;
+                                src = vrow<VT>(G, (uint32_t)par, d);
                                 b = vec_bytes;
                             } else {
                                 dst = drow + (size_t)pi * j * W;
@@ -1234,7 +1293,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
 #pragma unroll
                     for (int w = 0; w < WC; w++) {
                         const int t = 32 * w + (int)lane;
-                        const bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.pstride + t];
+                        const bool bit = t < d && S.q[t] >= to_f(prow[(size_t)pi * A.pstride + t]);
                         qb[w] = __ballot_sync(0xffffffffu, bit);
                     }
                     int c = 0;
@@ -1279,7 +1338,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                 for (int pi = 0; pi < gp; pi++)
                     for (int w = 0; w < W; w++) {
                         int t = 32 * w + (int)lane;
-                        bool bit = t < d && S.q[t] >= prow[(size_t)pi * A.pstride + t];
+                        bool bit = t < d && S.q[t] >= to_f(prow[(size_t)pi * A.pstride + t]);
                         unsigned word = __ballot_sync(0xffffffffu, bit);
                         if (lane == 0) qb[pi * W + w] = word;
                     }
@@ -1352,7 +1411,7 @@ static __device__ __noinline__ int64_t log_visits(int32_t* log, int64_t cap, con
 // One full search (search.py:269-335) over graph G.  Seeds (already in
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
-template <int D>
+template <int D, typename VT, int M>
 __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                            int ns, bool fill_random, Pcg64& rng, int64_t task,
                            int64_t* n_logged) {
@@ -1425,14 +1484,14 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     for (int it = 0; it < C.max_iter; it++) {
         S.c_it++;
         int inserted = 0;
-        if (A.prefetch && it > 0 && it < C.max_iter - 1) prefetch_parents<D>(A, S, G, C);
+        if (A.prefetch && it > 0 && it < C.max_iter - 1) prefetch_parents<D, VT>(A, S, G, C);
         if (n_new) {
             if (C.log && A.visit_log)
                 *n_logged = log_visits(A.visit_log + task * A.visit_cap, A.visit_cap, S.newl, n_new, *n_logged);
             S.c_dc += n_new;
             PW_T(7);
             const uint64_t thr = S.qlen == C.L ? S.qk0[C.L - 1] : ~0ull;
-            const int ns = score_rows<D>(A, S, G, n_new, thr);
+            const int ns = score_rows<D, VT, M>(A, S, G, n_new, thr);
             PW_T(1);
             inserted = merge_queue(A, S, C, ns);
             PW_T(2);
@@ -1450,7 +1509,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
             break;
         }
         S.c_ne += np;
-        int nc = expand<D>(A, S, G, C, parents, np, it, rng);
+        int nc = expand<D, VT>(A, S, G, C, parents, np, it, rng);
         PW_T(4);
         bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
         if (nc <= C.cap && !C.log)
@@ -1467,7 +1526,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     return converged;
 }
 
-template <int D>
+template <int D, typename VT, int M>
 __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const unsigned lane = lane_id();
@@ -1548,7 +1607,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
                 rng = A.rng_io ? A.rng_io[task]
                                : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)A.stage));
             }
-            converged = run_search<D>(A, S, gph ? A.ghost : G, gph ? A.gcfg : A.cfg, ns, fill_random,
+            converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G, gph ? A.gcfg : A.cfg, ns, fill_random,
                                       rng, task, &n_logged);
             if (gph) {
                 entry = A.ghost.gid[(uint32_t)S.qk_cur()[0]];
@@ -1570,7 +1629,9 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
             uint64_t key = qk[t];
             uint32_t loc = (uint32_t)key;
             A.out_ids[task * A.out_stride + t] = G.gid[loc];
-            A.out_dists[task * A.out_stride + t] = __fsqrt_rn(__uint_as_float((uint32_t)(key >> 32)));
+            // search.py:325 sqrt of the squared L2; IP reports the distance itself
+            const float dk = bits_dist<M>((uint32_t)(key >> 32));
+            A.out_dists[task * A.out_stride + t] = M == 0 ? __fsqrt_rn(dk) : dk;
             if (A.out_local) A.out_local[task * A.out_stride + t] = (int32_t)loc;
         }
         if (lane == 0) {

@@ -13,6 +13,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/pw_b200.h"
@@ -82,14 +83,48 @@ bool make_plan(int d, L2Plan& P) {
 // compile-time pairwise order); any other d runs the generic instance.
 // (PW_DIMS must match paper_2507_17094_b200/build_ext.py DIMS)
 #define PW_DIMS(X) X(16) X(32) X(64) X(96) X(100) X(128) X(200) X(256) X(384) X(512) X(768) X(960) X(1024)
+// uint8 rows: single-leaf specialisations with 16-byte rows (d <= 128, d % 16 == 0)
+#define PW_DIMS_U8(X) X(96) X(128)
+// inner product (float32 rows)
+#define PW_DIMS_IP(X) X(96) X(128) X(200)
 typedef KernelFn kernel_fn;
 }  // namespace
 #define PW_DECL(v) KernelFn pw_kernel_##v();
+#define PW_DECL_U8(v) KernelFn pw_kernel_u8_##v();
+#define PW_DECL_IP(v) KernelFn pw_kernel_ip_##v();
 PW_DIMS(PW_DECL)
+PW_DIMS_U8(PW_DECL_U8)
+PW_DIMS_IP(PW_DECL_IP)
 KernelFn pw_kernel_0();
+KernelFn pw_kernel_u8_0();
+KernelFn pw_kernel_ip_0();
 #undef PW_DECL
+#undef PW_DECL_U8
+#undef PW_DECL_IP
 namespace {
-kernel_fn pick_kernel(int d) {
+kernel_fn pick_kernel(int d, int dtype, int metric) {
+    if (metric == PW_METRIC_IP) {
+        switch (d) {
+#define PW_CASE(v) \
+    case v:        \
+        return pw_kernel_ip_##v();
+            PW_DIMS_IP(PW_CASE)
+#undef PW_CASE
+            default:
+                return pw_kernel_ip_0();
+        }
+    }
+    if (dtype == PW_DTYPE_U8) {
+        switch (d) {
+#define PW_CASE(v) \
+    case v:        \
+        return pw_kernel_u8_##v();
+            PW_DIMS_U8(PW_CASE)
+#undef PW_CASE
+            default:
+                return pw_kernel_u8_0();
+        }
+    }
     switch (d) {
 #define PW_CASE(v) \
     case v:        \
@@ -100,6 +135,7 @@ kernel_fn pick_kernel(int d) {
             return pw_kernel_0();
     }
 }
+bool is_generic(kernel_fn f) { return f == pw_kernel_0() || f == pw_kernel_u8_0() || f == pw_kernel_ip_0(); }
 
 struct DevInfo {
     int sms = 0;
@@ -119,10 +155,24 @@ int dev_info(int dev, DevInfo** out) {
     if (!I.attr_set) {
         PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_0(),
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+        PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_0(),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+        PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_0(),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
 #define PW_ATTR(v)                                                                             \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_##v(),                                 \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS(PW_ATTR)
+#undef PW_ATTR
+#define PW_ATTR(v)                                                                             \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_##v(),                              \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+        PW_DIMS_U8(PW_ATTR)
+#undef PW_ATTR
+#define PW_ATTR(v)                                                                             \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_##v(),                              \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+        PW_DIMS_IP(PW_ATTR)
 #undef PW_ATTR
         I.attr_set = true;
     }
@@ -136,14 +186,14 @@ struct pw_shard {
     int device = 0;
     int64_t n = 0;
     int32_t d = 0, j = 0, W = 0, dtype = 0;
-    float* vec = nullptr;
+    void* vec = nullptr;          // (n, d) f32 or u8 rows (dtype)
     int32_t* adj = nullptr;
     int32_t* gid = nullptr;
     uint32_t* dir = nullptr;
     int32_t* inter = nullptr;
     int64_t gn = 0;
     int32_t gj = 0;
-    float* gvec = nullptr;
+    void* gvec = nullptr;
     int32_t* gadj = nullptr;
     int32_t* gids = nullptr;
     int64_t bytes = 0;
@@ -174,13 +224,13 @@ int upload(T** dst, const void* src, size_t count, int64_t* bytes, bool on_devic
     return 0;
 }
 
-__global__ void gather_rows_kernel(const float* __restrict__ vec, const int32_t* __restrict__ ids,
-                                   int64_t n_ids, int32_t d, float* __restrict__ out) {
-    int64_t total = n_ids * d;
+__global__ void gather_rows_kernel(const uint8_t* __restrict__ vec, const int32_t* __restrict__ ids,
+                                   int64_t n_ids, int64_t row_bytes, uint8_t* __restrict__ out) {
+    int64_t total = n_ids * row_bytes;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = i / d, c = i % d;
-        out[i] = vec[(int64_t)ids[r] * d + c];
+        int64_t r = i / row_bytes, c = i % row_bytes;
+        out[i] = vec[(int64_t)ids[r] * row_bytes + c];
     }
 }
 
@@ -202,7 +252,9 @@ __global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float*
             bool f = id >= 0;
             unsigned b = __ballot_sync(0xffffffffu, f);
             int pos = cnt + __popc(b & lanemask_lt());
-            if (f) keys[pos] = ((uint64_t)__float_as_uint(dists[qi * n + t]) << 32) | (uint32_t)id;
+            // order-preserving bits (IP distances can be negative; for L2's
+            // non-negative values this is the plain float order too)
+            if (f) keys[pos] = ((uint64_t)dist_bits<1>(dists[qi * n + t]) << 32) | (uint32_t)id;
             cnt += __popc(b);
         }
         __syncwarp();
@@ -218,7 +270,7 @@ __global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float*
             for (int o = 0; o < cnt; o++) rank += keys[o] < key;
             if (rank < k) {
                 out_ids[qi * k + rank] = (int32_t)(uint32_t)key;
-                out_dists[qi * k + rank] = __uint_as_float((uint32_t)(key >> 32));
+                out_dists[qi * k + rank] = bits_dist<1>((uint32_t)(key >> 32));
             }
         }
         __syncwarp();
@@ -226,7 +278,8 @@ __global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float*
 }
 
 // Test hook: exact squared L2 of rows[ids] vs query (data.py:70-79).
-__global__ void l2_rows_kernel(const float* __restrict__ vec, int32_t d, int32_t spad, L2Plan plan,
+template <typename VT>
+__global__ void l2_rows_kernel(const VT* __restrict__ vec, int32_t d, int32_t spad, L2Plan plan,
                                const int32_t* __restrict__ ids, int64_t n_ids,
                                const float* __restrict__ query, float* __restrict__ out) {
     extern __shared__ float l2s[];
@@ -238,11 +291,11 @@ __global__ void l2_rows_kernel(const float* __restrict__ vec, int32_t d, int32_t
         __syncwarp();
         for (int v = 0; v < 4; v++) {
             int64_t r = r0 + v < n_ids ? r0 + v : n_ids - 1;
-            for (int t = lane; t < d; t += 32) rows[v * spad + t] = vec[(int64_t)ids[r] * d + t];
+            for (int t = lane; t < d; t += 32) rows[v * spad + t] = to_f(vec[(int64_t)ids[r] * d + t]);
         }
         __syncwarp();
         const unsigned v = lane >> 3, a = lane & 7u;
-        float dist = l2_row(plan, rows + v * spad, q, a);
+        float dist = l2_row<0, float>(plan, rows + v * spad, q, a);
         if (a == 0 && r0 + v < n_ids) out[r0 + v] = dist;
     }
 }
@@ -275,6 +328,7 @@ int validate_params(const pw_params& p) {  // search.py:58-70
     if (p.selection < 0 || p.selection > 2) return set_err(PW_EINVAL, "selection must be one of ('full', 'direction', 'random')");
     if (p.seed_mode < 0 || p.seed_mode > 1) return set_err(PW_EINVAL, "seed_mode must be one of ('neighbors', 'mixed')");
     if (p.buffer_cap < 0) return set_err(PW_EINVAL, "buffer_cap must be positive");
+    if (p.metric != PW_METRIC_L2 && p.metric != PW_METRIC_IP) return set_err(PW_EINVAL, "metric must be one of ('l2', 'ip')");
     return 0;
 }
 
@@ -297,7 +351,6 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
             int32_t n_seeds, bool ghost_on, Launch& Lc) {
     int rc = validate_params(p);
     if (rc) return rc;
-    if (sh->dtype != PW_DTYPE_F32) return set_err(PW_EINVAL, "only float32 shards are supported");
     KArgs& A = Lc.A;
     std::memset(&A, 0, sizeof A);
     A.main = GraphDev{sh->vec, sh->adj, sh->gid, sh->dir, (int32_t)sh->n, sh->j};
@@ -327,8 +380,27 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // ---- shared-memory layout per warp
     const int jm = std::max(G.j, ghost_on ? sh->gj : 0);
     const int d = sh->d;
-    int spad = (d + 31) / 32 * 32 + 8;  // == 8 mod 32: conflict-free (v, a) access
-    if (spad - 32 >= d) spad -= 32;
+    const int elem = sh->dtype == PW_DTYPE_U8 ? 1 : 4;  // bytes per vector element
+    int spad;
+    if (elem == 4) {
+        spad = (d + 31) / 32 * 32 + 8;  // == 8 mod 32 floats: conflict-free (v, a) access
+        if (spad - 32 >= d) spad -= 32;
+    } else {
+        // u8: 16-byte rows; the 8 rows of a pass read 8 bytes each (4 lanes x
+        // LDS.U16) -- pick a stride whose 8 row offsets hit distinct bank pairs
+        auto ok = [](int sp) {
+            uint32_t used = 0;
+            for (int v = 0; v < 8; v++) {
+                const int b = (v * sp / 4) % 32;
+                const uint32_t m = (1u << b) | (1u << ((b + 1) % 32));
+                if (used & m) return false;
+                used |= m;
+            }
+            return true;
+        };
+        spad = (d + 15) / 16 * 16;
+        while (!ok(spad)) spad += 16;
+    }
     A.spad = spad;
     int64_t cb = std::max<int64_t>({(int64_t)p.r * jm, (int64_t)A.cfg.want, (int64_t)1 + jm,
                                     (int64_t)n_seeds, (int64_t)A.gcfg.want, 32});
@@ -342,8 +414,10 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // by the per-warp epoch-tagged global table (batched probes): measured on
     // C2 (10M x 96, l=256) this fits ~10 query-warps per SM instead of 5 and
     // is faster for both the naive and the PathWeaver arm (profiles/r01).
-    Lc.fn = pick_kernel(d);
-    const bool specialised = Lc.fn != pw_kernel_0();
+    if (p.metric == PW_METRIC_IP && sh->dtype != PW_DTYPE_F32)
+        return set_err(PW_EINVAL, "inner-product search needs float32 vectors");
+    Lc.fn = pick_kernel(d, sh->dtype, p.metric);
+    const bool specialised = !is_generic(Lc.fn);
     // Specialised kernels keep the exact visited set only in the per-warp
     // epoch-tagged global table (batched probes; no shared table, which buys
     // resident warps).  The generic-d kernel uses a shared table spilling to
@@ -357,13 +431,18 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     int R;
     if (tun && tun->stage_rows > 0) {
         R = tun->stage_rows;
+    } else if (specialised && elem == 1) {
+        // u8 rows are small: fill the region the dedup hash needs anyway
+        // (8*BH + 4*CB bytes) with rows in flight, in 8-row compute passes
+        R = (int)std::max<int64_t>(16, (8 * (int64_t)A.BH + 4 * cb) / spad / 16 * 16);
+        R = std::min(R, 64);
     } else if (specialised) {
         // rows in flight per warp: two halves of 8 rows (one 8-row compute
         // pass each); large rows shrink to keep staging <= ~10 KB
         R = 16;
         while (R > 4 && (int64_t)R * spad * 4 > 10240) R >>= 1;
     } else {
-        R = std::max(2, std::min(16, (16384 / (spad * 4)) & ~1));
+        R = std::max(2, std::min(16, (16384 / (spad * elem)) & ~1));
     }
     R &= ~1;
     if (R < 2) R = 2;
@@ -372,10 +451,11 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // DGS parent rows are packed at a 16-byte stride (bit tests only, no
     // bank-conflict concern) so that kParentGroup parents fit the staging
     // ring and one expansion is ONE fetch round trip (C2: 8 x (96 + 96) words)
-    const int pstride = (d + 3) & ~3;
+    const int pstride = elem == 4 ? (d + 3) & ~3 : (d + 15) & ~15;  // elements, 16-byte rows
     if (A.cfg.prune_sel == PW_SEL_DIRECTION) {
-        while ((int64_t)R * spad < (int64_t)pstride + (int64_t)G.j * W) R += 2;
-        PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad) / (pstride + (int64_t)G.j * W));
+        const int64_t per = (int64_t)pstride * elem + 4ll * G.j * W;  // bytes per parent
+        while ((int64_t)R * spad * elem < per) R += 2;
+        PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad * elem) / per);
         PG = std::max(PG, 1);
     }
     A.R = R;
@@ -385,7 +465,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // between expansion and the visited filter, the staging ring only in
     // scoring and DGS expansion (before the dedup): they share one region.
     const int64_t hash_bytes = 8 * (int64_t)A.BH + 4 * cb;
-    const int64_t stage_bytes = std::max<int64_t>(4 * (int64_t)R * spad, hash_bytes);
+    const int64_t stage_bytes = std::max<int64_t>((int64_t)elem * R * spad, hash_bytes);
     // specialised kernels with j <= 32 keep the DGS counts/bits in registers
     const bool dgs_regs = specialised && G.j <= 32;
     auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
@@ -418,8 +498,11 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
     A.bulk_rows = 0;
     A.prefetch = (tun && (tun->flags & 1)) ? 1 : 0;
+    // flag 8: L2 warm-up of scoring rows two groups ahead (opt-in: measured
+    // slower at C2 -- 4.24 -> 4.69 ms PW, 5.65 -> 5.84 ms naive)
+    A.warm_rows = (tun && (tun->flags & 8)) ? 1 : 0;
     A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
-                  (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16(4ll * d) && b16(4ll * G.j * W))))
+                  (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16((int64_t)elem * d) && b16(4ll * G.j * W))))
                      ? ((tun && (tun->flags & 4)) ? 2 : 1)
                      : 0;
 
@@ -535,7 +618,10 @@ int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
     if (D->n <= 0) return set_err(PW_EINVAL, "empty graph");
     if (D->n >= (1ll << 31)) return set_err(PW_EINVAL, "shard too large (n_local >= 2^31)");
     if (D->d < 1 || D->j < 0) return set_err(PW_EINVAL, "bad dimensions");
-    if (D->dtype != PW_DTYPE_F32) return set_err(PW_EINVAL, "only float32 vectors are supported");
+    if (D->dtype != PW_DTYPE_F32 && D->dtype != PW_DTYPE_U8)
+        return set_err(PW_EINVAL, "vectors must be float32 or uint8");
+    if (D->dtype == PW_DTYPE_U8 && D->d % 4 != 0)
+        return set_err(PW_EINVAL, "uint8 vectors need d % 4 == 0 (4-byte row copies)");
     pw_shard* sh = new pw_shard();
     int dev = 0;
     cudaGetDevice(&dev);
@@ -551,7 +637,9 @@ int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
         return code;
     };
     const bool od = D->on_device != 0;
-    if ((rc = upload(&sh->vec, D->vectors, (size_t)D->n * D->d, &sh->bytes, od))) return fail(rc);
+    const size_t elem = D->dtype == PW_DTYPE_U8 ? 1 : 4;
+    if ((rc = upload((uint8_t**)&sh->vec, D->vectors, (size_t)D->n * D->d * elem, &sh->bytes, od)))
+        return fail(rc);
     if ((rc = upload(&sh->adj, D->adj, (size_t)D->n * D->j, &sh->bytes, od))) return fail(rc);
     if ((rc = upload(&sh->gid, D->global_ids, (size_t)D->n, &sh->bytes, od))) return fail(rc);
     if (D->direction &&
@@ -565,8 +653,10 @@ int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
         if ((rc = upload(&sh->gids, D->ghost_ids, (size_t)D->ghost_n, &sh->bytes, od))) return fail(rc);
         if ((rc = upload(&sh->gadj, D->ghost_adj, (size_t)D->ghost_n * D->ghost_j, &sh->bytes, od)))
             return fail(rc);
-        if ((rc = upload(&sh->gvec, nullptr, (size_t)D->ghost_n * D->d, &sh->bytes))) return fail(rc);
-        gather_rows_kernel<<<256, 256>>>(sh->vec, sh->gids, sh->gn, sh->d, sh->gvec);
+        if ((rc = upload((uint8_t**)&sh->gvec, nullptr, (size_t)D->ghost_n * D->d * elem, &sh->bytes)))
+            return fail(rc);
+        gather_rows_kernel<<<256, 256>>>((const uint8_t*)sh->vec, sh->gids, sh->gn, (int64_t)sh->d * elem,
+                                         (uint8_t*)sh->gvec);
         g_launches++;
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return fail(set_err(PW_ECUDA, cudaGetErrorString(e)));
@@ -883,7 +973,7 @@ int pw_launch_config(pw_shard* sh, const pw_params* params, const pw_tuning* tun
     out[1] = Lc.A.warp_bytes;
     out[2] = Lc.A.H;
     out[3] = Lc.A.R;
-    out[4] = Lc.fn == pw_kernel_0() ? 0 : sh->d;
+    out[4] = is_generic(Lc.fn) ? 0 : sh->d;
     out[5] = Lc.blocks;
     return 0;
 }
@@ -897,11 +987,17 @@ int pw_squared_l2_rows(pw_shard* sh, const int32_t* ids, int64_t n_ids, const fl
     int spad = (sh->d + 31) / 32 * 32 + 8;
     if (spad - 32 >= sh->d) spad -= 32;
     size_t smem = sizeof(float) * (((sh->d + 3) & ~3) + 4 * spad);
-    if (smem > 48 * 1024)
-        PW_CUDA(cudaFuncSetAttribute(l2_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int blocks = (int)std::min<int64_t>(4096, (n_ids + 3) / 4);
-    l2_rows_kernel<<<blocks, 32, smem, (cudaStream_t)stream>>>(sh->vec, sh->d, spad, plan, ids, n_ids,
+    auto go = [&](auto* tag) -> int {
+        using VT_ = std::remove_pointer_t<decltype(tag)>;
+        if (smem > 48 * 1024)
+            PW_CUDA(cudaFuncSetAttribute(l2_rows_kernel<VT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int blocks = (int)std::min<int64_t>(4096, (n_ids + 3) / 4);
+        l2_rows_kernel<VT_><<<blocks, 32, smem, (cudaStream_t)stream>>>((const VT_*)sh->vec, sh->d, spad, plan, ids, n_ids,
                                                                query, out);
+        return 0;
+    };
+    int rc_ = sh->dtype == PW_DTYPE_U8 ? go((uint8_t*)nullptr) : go((float*)nullptr);
+    if (rc_) return rc_;
     g_launches++;
     PW_CUDA(cudaGetLastError());
     return 0;

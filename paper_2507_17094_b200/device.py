@@ -32,7 +32,10 @@ class TensorShard:
         lib = _abi.load()
         torch.cuda.set_device(vectors.device)
         self.device = vectors.device
-        vec = vectors.contiguous().float()
+        # uint8 rows stay uint8 on the device (the reference upcasts them,
+        # data.py:36; float(b) is exact); anything else is float32
+        vec = vectors.contiguous() if vectors.dtype == torch.uint8 else vectors.contiguous().float()
+        self.dtype = "u8" if vec.dtype == torch.uint8 else "f32"
         adj = adj.contiguous().to(torch.int32)
         gid = global_ids.contiguous().to(torch.int32)
         dr = None if direction is None else direction.contiguous().to(torch.int32)
@@ -40,7 +43,8 @@ class TensorShard:
         gi = None if ghost_ids is None else ghost_ids.contiguous().to(torch.int32)
         ga = None if ghost_adj is None else ghost_adj.contiguous().to(torch.int32)
         torch.cuda.synchronize(self.device)
-        desc = _abi.ShardDesc(vec.shape[0], vec.shape[1], adj.shape[1], 0, _ptr(vec), _ptr(adj),
+        desc = _abi.ShardDesc(vec.shape[0], vec.shape[1], adj.shape[1], 1 if self.dtype == "u8" else 0,
+                              _ptr(vec), _ptr(adj),
                               _ptr(gid), _ptr(dr), _ptr(it), 0 if gi is None else gi.shape[0],
                               0 if ga is None else ga.shape[1], _ptr(gi), _ptr(ga), 1)
         h = C.c_void_p()

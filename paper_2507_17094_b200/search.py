@@ -39,6 +39,9 @@ class SearchParams:
     seed_mode: str = "neighbors"
     buffer_cap: int | None = None
     log_visits: bool = False
+    # extension beyond the reference (BASELINE C5): "ip" = inner product,
+    # distance -(q . x) in the same pairwise order; "l2" is the reference's
+    metric: str = "l2"
 
     def __post_init__(self):
         if not (1 <= self.k <= self.l and 1 <= self.r <= self.l):
@@ -53,6 +56,8 @@ class SearchParams:
             raise ValueError(f"selection must be one of {SELECTION_MODES}")
         if self.seed_mode not in SEED_MODES:
             raise ValueError(f"seed_mode must be one of {SEED_MODES}")
+        if self.metric not in ("l2", "ip"):
+            raise ValueError("metric must be one of ('l2', 'ip')")
 
     def with_(self, **kw) -> "SearchParams":
         return replace(self, **kw)
@@ -125,17 +130,40 @@ class ShardContext:
         return ShardContext(vectors=g.vectors, adj=g.adj, global_ids=g.parent_ids)
 
 
-class DeviceShard:
-    """Owner of one ``pw_shard`` (device copies of a ShardContext)."""
+def byte_rows(vec: np.ndarray) -> bool:
+    """True when float32 rows hold only integers in [0, 255] (SIFT-style
+    bvecs the reference upcast, data.py:36): the device can keep them as
+    uint8 -- 4x fewer gather bytes -- and float(b) recovers every value
+    exactly, so distances stay bit-identical."""
+    if vec.dtype == np.uint8:
+        return vec.shape[1] % 4 == 0
+    if vec.shape[1] % 4 != 0 or vec.size == 0:
+        return False
+    return bool(np.all((vec >= 0) & (vec <= 255) & (vec == np.floor(vec))))
 
-    def __init__(self, ctx, device: int | None = None):
+
+class DeviceShard:
+    """Owner of one ``pw_shard`` (device copies of a ShardContext).
+
+    storage: "auto" keeps byte-valued rows as uint8 on the device
+    (``byte_rows``), "f32" always uploads float32, "u8" requires byte rows."""
+
+    def __init__(self, ctx, device: int | None = None, storage: str = "auto"):
         import torch
 
         lib = _abi.load()
         if device is not None:
             torch.cuda.set_device(device)
         self.device = torch.cuda.current_device()
-        vec = np.ascontiguousarray(ctx.vectors, np.float32)
+        raw = np.asarray(ctx.vectors)
+        if storage not in ("auto", "f32", "u8"):
+            raise ValueError("storage must be one of ('auto', 'f32', 'u8')")
+        u8 = storage != "f32" and byte_rows(raw)
+        if storage == "u8" and not u8:
+            raise ValueError("storage='u8' needs integer rows in [0, 255] with d % 4 == 0")
+        vec = np.ascontiguousarray(raw, np.float32)
+        vdev = np.ascontiguousarray(raw, np.uint8) if u8 else vec
+        self.dtype = "u8" if u8 else "f32"
         adj = np.ascontiguousarray(ctx.adj, np.int32)
         if adj.ndim != 2:
             adj = adj.reshape(vec.shape[0], -1)
@@ -154,7 +182,7 @@ class DeviceShard:
         if vec.shape[0] == 0:
             raise ValueError("empty graph")
         desc = _abi.ShardDesc(
-            vec.shape[0], vec.shape[1], adj.shape[1], 0, vec.ctypes.data, adj.ctypes.data,
+            vec.shape[0], vec.shape[1], adj.shape[1], 1 if u8 else 0, vdev.ctypes.data, adj.ctypes.data,
             gid.ctypes.data, None if direction is None else direction.ctypes.data,
             None if inter is None else inter.ctypes.data,
             0 if gids is None else gids.shape[0], 0 if gadj is None else gadj.shape[1],

@@ -1,0 +1,83 @@
+"""Inner-product metric (BASELINE C5, Text2Image-shaped).  The reference has
+only squared L2, so this is an extension with parity UNPINNED: the checker is
+the oracle's restatement (distance = -(pairwise_sum(x * q)), same float32
+order, no FMA; oracle/pw_oracle.c neg_ip_row).  Everything else -- queue,
+DGS, ghost staging, ring, counters -- is the reference's path unchanged."""
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2507_17094_b200 as pw
+from golden_util import assert_run_equal, assert_run_equal_lossy, oracle_dict, result_dict
+from index_util import clustered, make_contexts
+from paper_2507_17094_b200.rng import TAG_SEARCH, stream
+from paper_2507_17094_b200.search import SearchParams
+
+pytestmark = pytest.mark.gpu
+
+
+def unit_rows(n, d, seed):
+    x = clustered(n, d, 128, 0.15, seed=seed) - np.float32(0.5)
+    return (x / np.linalg.norm(x, axis=1, keepdims=True)).astype(np.float32)
+
+
+@pytest.fixture(scope="module")
+def ipsets():
+    out = {}
+    # 200: Text2Image shape (specialised IP kernel); 96 / 128 specialised; 40 generic
+    for d, n, nq, shards in ((200, 8000, 200, 2), (96, 12000, 300, 2), (128, 8000, 200, 3),
+                             (40, 6000, 200, 2)):
+        x = unit_rows(n + nq, d, seed=d + 11)
+        out[d] = (np.ascontiguousarray(x[n:]), make_contexts(x[:n], shards, 32, seed=d))
+    return out
+
+
+ARMS = [
+    dict(k=10, l=64, m=64, r=8, max_iter=64, seed=1, metric="ip"),
+    dict(k=100, l=128, m=64, r=8, max_iter=64, seed=2, selection="direction", discard_ratio=0.5,
+         cooldown_ratio=0.3, ghost_enabled=True, ghost_max_iter=8, metric="ip"),
+    dict(k=10, l=96, m=64, r=4, max_iter=10, seed=3, selection="random", discard_ratio=0.5,
+         seed_mode="mixed", ghost_enabled=True, metric="ip"),
+]
+
+
+@pytest.mark.parametrize("d", [200, 96, 128, 40])
+@pytest.mark.parametrize("arm", range(len(ARMS)))
+@pytest.mark.parametrize("mode", ["baseline", "pipelined"])
+def test_ip_matches_oracle(ipsets, d, arm, mode):
+    queries, ctxs = ipsets[d]
+    params = SearchParams(**ARMS[arm])
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(pw.Dataset(queries), None, None, params, contexts=ctxs))
+    want = oracle_dict(oracle.run(queries, ctxs, params, mode))
+    assert_run_equal(got, want, f"ip d={d} arm={arm} {mode}")
+    fd = np.where(np.isfinite(got["final_dists"]), got["final_dists"], np.float32(3e38))
+    assert np.all(np.diff(fd, axis=1) >= 0)  # ascending -(q.x), +inf padding last
+    lossy = result_dict(runner(pw.Dataset(queries), None, None, params, contexts=ctxs,
+                               tuning={"flags": 2}))
+    assert_run_equal_lossy(lossy, want, f"ip lossy d={d} arm={arm} {mode}")
+
+
+def test_ip_single_search_matches_oracle(ipsets):
+    queries, ctxs = ipsets[200]
+    params = SearchParams(k=10, l=64, m=32, r=4, max_iter=30, seed=9, metric="ip")
+    for qi in range(5):
+        g1 = stream(9, TAG_SEARCH, qi, 0)
+        got = pw.search(queries[qi], ctxs[0], params, rng=g1, query_id=qi)
+        g2 = stream(9, TAG_SEARCH, qi, 0)
+        want, _ = oracle.search(queries[qi], ctxs[0], params, rng_state=g2.bit_generator.state)
+        assert np.array_equal(got.ids, want["ids"])
+        assert np.array_equal(got.dists, want["dists"])
+        assert got.counters.distance_computations == want["counters"]["distance_computations"]
+
+
+def test_ip_top1_is_max_inner_product(ipsets):
+    """Sanity of the metric itself: on a complete graph the search is exact."""
+    x = unit_rows(300, 200, seed=5)
+    q = unit_rows(1, 200, seed=6)[0]
+    adj = np.array([[j for j in range(300) if j != i] for i in range(300)], np.int32)
+    ctx = pw.ShardContext(vectors=x, adj=adj, global_ids=np.arange(300, dtype=np.int32))
+    params = SearchParams(k=5, l=300, m=300, r=1, max_iter=3, seed=1, metric="ip")
+    res = pw.search(q, ctx, params, rng=stream(1, TAG_SEARCH, 0, 0))
+    assert res.ids[0] == int(np.argmax(x @ q))
