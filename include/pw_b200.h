@@ -172,6 +172,36 @@ int pw_run_device(pw_shard* const* shards, int32_t n_shards, const pw_params* pa
                   float* final_dists, int32_t* stats_i32, int64_t* stats_i64,
                   int32_t* entries_a, int32_t* entries_b, void* stream);
 
+/* Dataflow ring: the pipelined path extension of pipeline.py:308-347 as ONE
+ * persistent K1 launch per shard.  Shard g runs every (stage s, query q) task
+ * with chunk(q) = (g - s) mod N in stage-major order; a stage s > 0 task
+ * waits on inbox[q] (epoch << 32 | entry) and a finished stage s < N-1 task
+ * stores epoch << 32 | inter_map[top1] into next_inbox[q] -- shard g+1's
+ * inbox, a peer (NVLink) mapping when the shards live on different GPUs
+ * (pw_ipc_*), so stage boundaries never stop a GPU.  Outputs may also be
+ * peer mappings (the reducing rank's buffers): shard_ids/dists (q, N, k)
+ * column g; stats_i32 (N, 4, q) / stats_i64 (N, 6, q) row `stage`.
+ * epoch: a run tag equal on every shard, new for every run (inboxes are
+ * never reset).  sm_limit > 0 caps the CTAs (several shards sharing one GPU
+ * must all be resident).  Device pointers; asynchronous on `stream`. */
+int pw_search_dataflow(pw_shard* shard, const pw_params* params, const pw_tuning* tuning,
+                       const float* queries, int64_t q, int32_t g, int32_t n_shards,
+                       uint32_t epoch, const uint64_t* inbox, uint64_t* next_inbox,
+                       int32_t* shard_ids, float* shard_dists, int32_t* stats_i32,
+                       int64_t* stats_i64, int32_t sm_limit, void* stream);
+
+/* Synchronous check of a shard's device error flag (table overflow, a
+ * dataflow inbox that never filled); clears it.  0 or PW_ECUDA + message. */
+int pw_shard_check(pw_shard* shard);
+
+/* Device buffers shareable across processes (cudaMalloc'd, so an IPC handle
+ * maps exactly this allocation) and their CUDA IPC handles (64 bytes). */
+int pw_dev_alloc(int64_t bytes, void** out);
+int pw_dev_free(void* ptr);
+int pw_ipc_get(const void* ptr, void* handle64);
+int pw_ipc_open(const void* handle64, void** out);
+int pw_ipc_close(void* ptr);
+
 /* Bit-exact data.py:70-79 squared_l2 of rows[ids] against one query, on the
  * device (test hook for the distance primitive).  Device pointers. */
 int pw_squared_l2_rows(pw_shard* shard, const int32_t* ids, int64_t n_ids,

@@ -82,9 +82,20 @@ EXPORTS = {
                                      C.c_void_p]),
     "pw_launch_config": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(Tuning), C.c_void_p]),
     "pw_phase_cycles": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    "pw_search_dataflow": (C.c_int, [C.c_void_p, C.POINTER(Params), C.POINTER(Tuning), C.c_void_p,
+                                     C.c_int64, C.c_int32, C.c_int32, C.c_uint32, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_int32, C.c_void_p]),
+    "pw_shard_check": (C.c_int, [C.c_void_p]),
+    "pw_dev_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    "pw_dev_free": (C.c_int, [C.c_void_p]),
+    "pw_ipc_get": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "pw_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    "pw_ipc_close": (C.c_int, [C.c_void_p]),
 }
 
-OPTIONAL = {"pw_phase_cycles", "pw_launch_config"}
+OPTIONAL = {"pw_phase_cycles", "pw_launch_config", "pw_search_dataflow", "pw_shard_check", "pw_dev_alloc", "pw_dev_free",
+            "pw_ipc_get", "pw_ipc_open", "pw_ipc_close"}
 _LIB = None
 
 

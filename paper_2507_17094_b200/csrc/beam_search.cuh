@@ -112,7 +112,29 @@ struct KArgs {
     int64_t gscratch_words;
     int32_t* task_counter;
     int32_t* err;
+    // Dataflow ring (pw_search_dataflow): one persistent launch per shard runs
+    // every (stage, query) task of shard g in stage-major order; a stage-s>0
+    // task waits for its entry, which shard g-1 stores straight into this
+    // shard's inbox (P2P over NVLink between GPUs) when its stage s-1 search
+    // ends -- no stage barriers, no host round trips (pipeline.py:327-347).
+    int32_t df;             // 1: dataflow task mapping
+    int32_t df_g, df_N;
+    int32_t df_lo[9];       // chunk bounds, np.array_split(arange(Q), N) (pipeline.py:327)
+    int32_t df_base[9];     // first task of each stage on this shard
+    uint32_t df_epoch;      // run tag carried by inbox words (no reset between runs)
+    const unsigned long long* df_inbox;  // (Q,) epoch << 32 | entry, written by shard g-1
+    unsigned long long* df_next;         // shard g+1's inbox (peer mapping or local)
+    int64_t st32_stage_stride, st64_stage_stride;  // stats (stage, f, q) = stage*stride + f*st_stride + q
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -1564,16 +1586,46 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         if (lane == 0) task = atomicAdd(A.task_counter, 1);
         task = __shfl_sync(0xffffffffu, task, 0);
         if (task >= A.n_tasks) break;
-        const int64_t qid = A.q0 + task;
+        int64_t qid = A.q0 + task;
+        int64_t row = task;  // query / output / stats row
+        int32_t stage = A.stage;
+        bool has_entry = A.entries != nullptr;
+        int32_t entry = has_entry ? A.entries[task] : -1;
+        if (A.df) {
+            // stage-major task list of shard g: stage s searches chunk (g - s) mod N
+            stage = 0;
+            while (stage + 1 < A.df_N && task >= A.df_base[stage + 1]) stage++;
+            const int c = (A.df_g - stage + A.df_N) % A.df_N;
+            qid = A.df_lo[c] + (task - A.df_base[stage]);
+            row = qid;
+            has_entry = stage > 0;
+            if (has_entry) {
+                unsigned long long v = 0;
+                if (lane == 0) {
+                    // bounded wait (~10 s): a producer that never comes (a
+                    // shard not resident, a dead peer) raises an error
+                    // instead of hanging the GPU
+                    for (uint32_t spin = 0;; spin++) {
+                        v = ld_acquire_sys(A.df_inbox + qid);
+                        if ((uint32_t)(v >> 32) == A.df_epoch) break;
+                        if (spin > (1u << 25)) {
+                            atomicOr(A.err, 16);
+                            v = 0;
+                            break;
+                        }
+                        __nanosleep(256);
+                    }
+                }
+                entry = (int32_t)(uint32_t)__shfl_sync(0xffffffffu, (unsigned)v, 0);
+            }
+        }
         // query row -> smem
-        for (int t = lane; t < A.d; t += 32) S.q[t] = A.queries[(size_t)task * A.d + t];
+        for (int t = lane; t < A.d; t += 32) S.q[t] = A.queries[(size_t)row * A.d + t];
         __syncwarp();
 
         int32_t g_it = 0;
         int64_t g_dc = 0, g_tv = 0, g_ne = 0;
         int64_t n_logged = 0;
-        bool has_entry = A.entries != nullptr;
-        int32_t entry = has_entry ? A.entries[task] : -1;
         const GraphDev& G = A.use_ghost_graph ? A.ghost : A.main;
 
         // Phase 0 = ghost staging (pipeline.py:218-226) when the task has no
@@ -1587,7 +1639,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
             bool fill_random = true;
             Pcg64 rng;
             if (gph) {
-                rng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)A.stage));
+                rng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)stage));
             } else {
                 // seeds (pipeline.py:227-231, search.py:294)
                 if (A.n_seeds > 0) {
@@ -1605,7 +1657,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
                 }
                 __syncwarp();
                 rng = A.rng_io ? A.rng_io[task]
-                               : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)A.stage));
+                               : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)stage));
             }
             converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G, gph ? A.gcfg : A.cfg, ns, fill_random,
                                       rng, task, &n_logged);
@@ -1628,13 +1680,39 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         for (int t = lane; t < nk; t += 32) {
             uint64_t key = qk[t];
             uint32_t loc = (uint32_t)key;
-            A.out_ids[task * A.out_stride + t] = G.gid[loc];
+            A.out_ids[row * A.out_stride + t] = G.gid[loc];
             // search.py:325 sqrt of the squared L2; IP reports the distance itself
             const float dk = bits_dist<M>((uint32_t)(key >> 32));
-            A.out_dists[task * A.out_stride + t] = M == 0 ? __fsqrt_rn(dk) : dk;
-            if (A.out_local) A.out_local[task * A.out_stride + t] = (int32_t)loc;
+            A.out_dists[row * A.out_stride + t] = M == 0 ? __fsqrt_rn(dk) : dk;
+            if (A.out_local) A.out_local[row * A.out_stride + t] = (int32_t)loc;
         }
-        if (lane == 0) {
+        if (A.df) {
+            // short lists padded -1 / +inf here (pipeline.py:244-246): the
+            // output may be another GPU's buffer, written by nobody else
+            for (int t = nk + lane; t < A.cfg.k; t += 32) {
+                A.out_ids[row * A.out_stride + t] = -1;
+                A.out_dists[row * A.out_stride + t] = __int_as_float(0x7f800000);
+            }
+            if (lane == 0) {
+                if (stage + 1 < A.df_N)  // pipeline.py:339 forward inter_map[top1] to shard g+1
+                    st_release_sys(A.df_next + qid, ((unsigned long long)A.df_epoch << 32) |
+                                                        (uint32_t)(nk > 0 ? A.inter[(uint32_t)qk[0]] : 0));
+                if (A.st32) {
+                    int32_t* s32 = A.st32 + stage * A.st32_stage_stride + qid;
+                    int64_t* s64 = A.st64 + stage * A.st64_stage_stride + qid;
+                    s32[0 * A.st_stride] = (int32_t)S.c_it;
+                    s32[1 * A.st_stride] = g_it;
+                    s32[2 * A.st_stride] = S.qlen;
+                    s32[3 * A.st_stride] = converged ? 1 : 0;
+                    s64[0 * A.st_stride] = S.c_dc + g_dc;
+                    s64[1 * A.st_stride] = S.c_tv + g_tv;
+                    s64[2 * A.st_stride] = S.c_ins;
+                    s64[3 * A.st_stride] = S.c_dgs;
+                    s64[4 * A.st_stride] = S.c_ne;
+                    s64[5 * A.st_stride] = g_ne;
+                }
+            }
+        } else if (lane == 0) {
             if (A.forward && nk > 0) A.forward[task] = A.inter[(uint32_t)qk[0]];
             if (A.st32) {
                 A.st32[0 * A.st_stride + task] += (int32_t)S.c_it;

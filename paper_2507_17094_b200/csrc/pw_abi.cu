@@ -587,7 +587,8 @@ int check_err(pw_shard* sh) {
     PW_CUDA(cudaMemcpy(&e, sh->counter + 1, sizeof e, cudaMemcpyDeviceToHost));
     if (e) {
         cudaMemset(sh->counter + 1, 0, sizeof(int32_t));
-        return set_err(PW_ECUDA, "beam_search_kernel internal table overflow (flag " + std::to_string(e) + ")");
+        return set_err(PW_ECUDA, (e & 16) ? std::string("dataflow inbox wait timed out (flag ") + std::to_string(e) + ")"
+                                          : "beam_search_kernel internal table overflow (flag " + std::to_string(e) + ")");
     }
     return 0;
 }
@@ -709,6 +710,94 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
     A.st64 = stats_i64 ? stats_i64 + q0 : nullptr;
     A.st_stride = q_total;
     return launch(sh, Lc, (cudaStream_t)stream);
+}
+
+int pw_search_dataflow(pw_shard* sh, const pw_params* params, const pw_tuning* tuning,
+                       const float* queries, int64_t q, int32_t g, int32_t N, uint32_t epoch,
+                       const uint64_t* inbox, uint64_t* next_inbox, int32_t* shard_ids,
+                       float* shard_dists, int32_t* stats_i32, int64_t* stats_i64, int32_t sm_limit,
+                       void* stream) {
+    if (!sh || !params) return set_err(PW_EINVAL, "null argument");
+    if (N < 1 || N > 8 || g < 0 || g >= N) return set_err(PW_EINVAL, "dataflow ring needs 1 <= N <= 8, 0 <= g < N");
+    if (q < 1 || q >= (1ll << 31)) return set_err(PW_EINVAL, "bad query count");
+    if (N > 1 && !sh->inter)
+        return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
+    if (N > 1 && (!inbox || !next_inbox)) return set_err(PW_EINVAL, "dataflow ring needs inboxes");
+    Launch Lc;
+    const bool ghost_on = params->ghost_enabled && sh->gn > 0;  // stage-0 tasks only
+    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc);
+    if (rc) return rc;
+    KArgs& A = Lc.A;
+    A.df = 1;
+    A.df_g = g;
+    A.df_N = N;
+    for (int c = 0; c <= N; c++) A.df_lo[c] = c == 0 ? 0 : A.df_lo[c - 1] + (int32_t)(q / N + (c - 1 < q % N ? 1 : 0));
+    A.df_base[0] = 0;
+    for (int st = 0; st < N; st++) {
+        const int c = ((g - st) % N + N) % N;
+        A.df_base[st + 1] = A.df_base[st] + (A.df_lo[c + 1] - A.df_lo[c]);
+    }
+    A.df_epoch = epoch;
+    A.df_inbox = reinterpret_cast<const unsigned long long*>(inbox);
+    A.df_next = reinterpret_cast<unsigned long long*>(next_inbox);
+    A.stage = 0;
+    A.q0 = 0;
+    A.n_tasks = (int32_t)q;
+    A.queries = queries;
+    A.entries = nullptr;
+    A.forward = nullptr;
+    const int64_t k = params->k;
+    A.out_ids = shard_ids + (int64_t)g * k;
+    A.out_dists = shard_dists + (int64_t)g * k;
+    A.out_local = nullptr;
+    A.out_stride = (int64_t)N * k;
+    A.st32 = stats_i32;
+    A.st64 = stats_i64;
+    A.st_stride = q;
+    if ((stats_i32 == nullptr) != (stats_i64 == nullptr))
+        return set_err(PW_EINVAL, "stats_i32 and stats_i64 go together");
+    A.st32_stage_stride = 4 * q;  // (N, 4, q)
+    A.st64_stage_stride = 6 * q;  // (N, 6, q)
+    if (sm_limit > 0) Lc.blocks = std::min(Lc.blocks, sm_limit);
+    return launch(sh, Lc, (cudaStream_t)stream);
+}
+
+int pw_shard_check(pw_shard* sh) {
+    if (!sh) return set_err(PW_EINVAL, "null argument");
+    if (!sh->counter) return 0;
+    PW_CUDA(cudaSetDevice(sh->device));
+    return check_err(sh);
+}
+
+int pw_dev_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 0) return set_err(PW_EINVAL, "bad argument");
+    *out = nullptr;
+    PW_CUDA(cudaMalloc(out, (size_t)std::max<int64_t>(bytes, 1)));
+    PW_CUDA(cudaMemset(*out, 0, (size_t)std::max<int64_t>(bytes, 1)));
+    return 0;
+}
+int pw_dev_free(void* ptr) {
+    if (ptr) PW_CUDA(cudaFree(ptr));
+    return 0;
+}
+int pw_ipc_get(const void* ptr, void* handle64) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handle size");
+    if (!ptr || !handle64) return set_err(PW_EINVAL, "null argument");
+    cudaIpcMemHandle_t h;
+    PW_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+    std::memcpy(handle64, &h, sizeof h);
+    return 0;
+}
+int pw_ipc_open(const void* handle64, void** out) {
+    if (!handle64 || !out) return set_err(PW_EINVAL, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    PW_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+    return 0;
+}
+int pw_ipc_close(void* ptr) {
+    if (ptr) PW_CUDA(cudaIpcCloseMemHandle(ptr));
+    return 0;
 }
 
 int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q, int32_t n_cand,

@@ -60,6 +60,11 @@ class TensorShard:
         self._finalizer = weakref.finalize(self, lib.pw_shard_destroy, h)
 
 
+def check_shard(shard: TensorShard) -> None:
+    """Raise if the shard's device error flag is set (synchronises)."""
+    _abi.check(_abi.load().pw_shard_check(shard.handle))
+
+
 class DeviceRun:
     """Preallocated device outputs for Q queries over n_cols shard columns."""
 
@@ -159,6 +164,90 @@ def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: st
                        forward_out=eout if stage < n - 1 else None)
             ein, eout = eout, ein
     reduce(run, stream)
+
+
+class DevArray:
+    """A pw_dev_alloc'd buffer (its own cudaMalloc, so a CUDA IPC handle maps
+    exactly it) or an IPC mapping of another process's buffer, viewed as a
+    torch tensor through __cuda_array_interface__ (no copy)."""
+
+    _TYPESTR = {torch.int32: "<i4", torch.int64: "<i8", torch.float32: "<f4", torch.uint64: "<u8"}
+
+    def __init__(self, shape, dtype, handle: bytes | None = None):
+        lib = _abi.load()
+        self.shape, self.dtype = tuple(shape), dtype
+        nbytes = int(np.prod(self.shape)) * torch.empty((), dtype=dtype).element_size()
+        ptr = C.c_void_p()
+        if handle is None:
+            _abi.check(lib.pw_dev_alloc(nbytes, C.byref(ptr)))
+            self._finalizer = weakref.finalize(self, lib.pw_dev_free, ptr.value)
+        else:
+            buf = C.create_string_buffer(bytes(handle), 64)
+            _abi.check(lib.pw_ipc_open(buf, C.byref(ptr)))
+            self._finalizer = weakref.finalize(self, lib.pw_ipc_close, ptr.value)
+        self.ptr = ptr.value
+        self.__cuda_array_interface__ = {"shape": self.shape, "typestr": self._TYPESTR[dtype],
+                                         "data": (self.ptr, False), "version": 3, "strides": None}
+        self.t = torch.as_tensor(self, device=torch.device("cuda", torch.cuda.current_device()))
+
+    def ipc_handle(self) -> bytes:
+        lib = _abi.load()
+        buf = C.create_string_buffer(64)
+        _abi.check(lib.pw_ipc_get(C.c_void_p(self.ptr), buf))
+        return buf.raw
+
+
+def search_dataflow(shard: TensorShard, params, queries: torch.Tensor, g: int, n: int, epoch: int,
+                    inbox: int | None, next_inbox: int | None, shard_ids: int, shard_dists: int,
+                    s32: int | None, s64: int | None, tuning=None, sm_limit: int = 0,
+                    stream=None) -> None:
+    """One pw_search_dataflow launch of shard g of an N-shard ring (device
+    pointers; the inbox / outputs may be peer mappings)."""
+    lib = _abi.load()
+    p = _abi.params_struct(params)
+    t = _abi.tuning_struct(tuning)
+    st = (stream or torch.cuda.current_stream(queries.device)).cuda_stream
+    _abi.check(lib.pw_search_dataflow(shard.handle, C.byref(p), C.byref(t), queries.data_ptr(),
+                                      queries.shape[0], g, n, epoch & 0xFFFFFFFF, inbox, next_inbox,
+                                      shard_ids, shard_dists, s32, s64, sm_limit, st))
+
+
+class LocalDataflow:
+    """The dataflow ring with all N shards on this GPU (logical shards): N
+    persistent launches on N streams, each capped to SMs/N CTAs so that all
+    are resident at once, entries handed over through device-memory inboxes.
+    The same protocol as the one-GPU-per-shard ring (ring.DataflowRing),
+    there over NVLink peer mappings."""
+
+    def __init__(self, shards: list, q: int, k: int, device):
+        self.shards = shards
+        self.n = len(shards)
+        dev = torch.device(device)
+        self.inbox = [torch.zeros(q, dtype=torch.int64, device=dev) for _ in range(self.n)]
+        self.streams = [torch.cuda.Stream(dev) for _ in range(self.n)]
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        self.sm_limit = max(1, sms // self.n)
+        self.epoch = 0
+
+    def run(self, params, queries: torch.Tensor, run: DeviceRun, tuning=None, stream=None) -> None:
+        stream = stream or torch.cuda.current_stream(queries.device)
+        self.epoch += 1
+        ready = torch.cuda.Event()
+        ready.record(stream)
+        done = []
+        for g, sh in enumerate(self.shards):
+            st = self.streams[g]
+            st.wait_event(ready)
+            search_dataflow(sh, params, queries, g, self.n, self.epoch, self.inbox[g].data_ptr(),
+                            self.inbox[(g + 1) % self.n].data_ptr(), run.shard_ids.data_ptr(),
+                            run.shard_dists.data_ptr(), run.s32.data_ptr(), run.s64.data_ptr(),
+                            tuning=tuning, sm_limit=self.sm_limit, stream=st)
+            ev = torch.cuda.Event()
+            ev.record(st)
+            done.append(ev)
+        for ev in done:
+            stream.wait_event(ev)
+        reduce(run, stream)
 
 
 def algorithmic_bytes(stats: list[dict], params, d: int, j: int, j_g: int, esize: int = 4,

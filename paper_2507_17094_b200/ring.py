@@ -196,3 +196,136 @@ class RingSearch:
         else:
             out["bytes_out"] = 0
         return out
+
+
+class DataflowRing:
+    """One shard per GPU, pipelined path extension WITHOUT stage barriers
+    (pw_search_dataflow): each rank runs one persistent K1 over all its
+    (stage, query) tasks; a finished stage-s search stores its entry
+    (inter_map[top1], pipeline.py:339) straight into rank g+1's inbox -- a
+    CUDA IPC peer mapping, so the 8-byte store travels over NVLink -- and
+    writes its candidate-list column and counters straight into rank 0's
+    result buffers.  The only host synchronisation per run is one barrier
+    before (rank 0's buffers are free again) and one after (all columns
+    landed); rank 0 then runs K2.  Baseline mode uses the same peer outputs
+    with one pw_search_stage launch per rank (no exchange at all).
+
+    torch.distributed (NCCL or gloo) only carries the 64-byte IPC handles
+    and the barriers.  Ranks may share a GPU (tests): pass sm_limit so every
+    rank's persistent kernel stays resident."""
+
+    def __init__(self, shard, q: int, k: int, rank: int, world: int, device, tuning=None,
+                 sm_limit: int = 0):
+        import torch
+        import torch.distributed as dist
+
+        from . import device as dv
+
+        self.shard, self.q, self.k, self.rank, self.world = shard, q, k, rank, world
+        self.tuning = tuning
+        self.dev = torch.device(device)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.sm_limit = sm_limit
+        self.epoch = 0
+        N = world
+        self.inbox = dv.DevArray((q,), torch.int64)
+        res = None
+        if rank == 0:
+            res = [dv.DevArray((q, N, k), torch.int32), dv.DevArray((q, N, k), torch.float32),
+                   dv.DevArray((N, 4, q), torch.int32), dv.DevArray((N, 6, q), torch.int64)]
+        handles = [None] * world
+        mine = {"inbox": self.inbox.ipc_handle(),
+                "res": [a.ipc_handle() for a in res] if res else None}
+        dist.all_gather_object(handles, mine)
+        nxt = (rank + 1) % world
+        self.next_inbox = self.inbox if nxt == rank else dv.DevArray((q,), torch.int64, handles[nxt]["inbox"])
+        if rank == 0:
+            self.res = res
+        else:
+            shapes = [((q, N, k), torch.int32), ((q, N, k), torch.float32), ((N, 4, q), torch.int32),
+                      ((N, 6, q), torch.int64)]
+            self.res = [dv.DevArray(sh, dt, h) for (sh, dt), h in zip(shapes, handles[0]["res"])]
+        self.final_ids = torch.empty((q, k), dtype=torch.int32, device=self.dev)
+        self.final_dists = torch.empty((q, k), dtype=torch.float32, device=self.dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    def run(self, queries, params, mode: str, timer: list | None = None):
+        """Search all queries (every rank passes the full (Q, d) device batch);
+        returns final ids (Q, k) numpy on rank 0, None elsewhere."""
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _abi
+        from . import device as dv
+
+        g, N = self.rank, self.world
+        ids, dists, s32, s64 = self.res
+        self.epoch += 1
+        if g == 0:
+            ids.t.fill_(-1)
+            dists.t.fill_(float("inf"))
+            s32.t.zero_()
+            s64.t.zero_()
+        torch.cuda.synchronize(self.dev)
+        dist.barrier()  # rank 0's result buffers are clean and free
+        e0 = e1 = None
+        if timer is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+        if mode == "baseline" or N == 1:
+            # pipeline.py:288-297: every rank searches every query at stage g
+            lib = _abi.load()
+            p = _abi.params_struct(params)
+            t = _abi.tuning_struct(self.tuning)
+            _abi.check(lib.pw_search_stage(self.shard.handle, C.byref(p), C.byref(t), queries.data_ptr(),
+                                           0, self.q, g, None, None, ids.ptr, dists.ptr, N, g,
+                                           s32.ptr + g * 4 * self.q * 4, s64.ptr + g * 6 * self.q * 8,
+                                           self.q, self.stream.cuda_stream))
+        else:
+            dv.search_dataflow(self.shard, params, queries, g, N, self.epoch, self.inbox.ptr,
+                               self.next_inbox.ptr, ids.ptr, dists.ptr, s32.ptr, s64.ptr,
+                               tuning=self.tuning, sm_limit=self.sm_limit, stream=self.stream)
+        if timer is not None:
+            e1.record(self.stream)
+            timer.append((e0, e1))
+        torch.cuda.synchronize(self.dev)
+        dv.check_shard(self.shard)
+        dist.barrier()  # every column and counter has landed in rank 0's buffers
+        if g != 0:
+            return None
+        lib = _abi.load()
+        _abi.check(lib.pw_reduce_topk(ids.ptr, dists.ptr, self.q, N * self.k, self.k,
+                                      self.final_ids.data_ptr(), self.final_dists.data_ptr(),
+                                      self.err.data_ptr(), self.stream.cuda_stream))
+        return self.final_ids.cpu().numpy()
+
+    def last_stats(self) -> list[dict]:
+        from .device import STAT_I32, STAT_I64
+
+        if self.rank != 0:
+            return []
+        s32 = self.res[2].t.cpu().numpy()
+        s64 = self.res[3].t.cpu().numpy()
+        out = []
+        for s in range(self.world):
+            st = {name: s32[s, i] for i, name in enumerate(STAT_I32)}
+            st.update({name: s64[s, i] for i, name in enumerate(STAT_I64)})
+            out.append(st)
+        return out
+
+    def run_host(self, queries_host: np.ndarray, params) -> dict:
+        """End to end: host queries in (H2D), final lists out on rank 0 (D2H)."""
+        import torch
+
+        qd = torch.from_numpy(queries_host).to(self.dev, non_blocking=False)
+        ids = self.run(qd, params, "pipelined")
+        out = {"final_ids": ids}
+        if self.rank == 0:
+            out["final_dists"] = self.final_dists.cpu().numpy()
+            out["bytes_out"] = out["final_ids"].nbytes + out["final_dists"].nbytes
+        else:
+            out["bytes_out"] = 0
+        return out
