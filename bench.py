@@ -61,7 +61,7 @@ CONFIGS = {
                rho=0.01, j_g=16, probe=48),
     "c5s": dict(workload="Text2Image-shaped 12.5M x 200 f32 inner product (one of C5's 8 shards of "
                          "100M), 10K queries, k=100, degree-32 graph", n=12_500_000, d=200, nq=10_000,
-                k=100, j=32, gen="latent", m=24, n_clusters=1, spread=1.0, noise=0.05, rho=0.01,
+                k=100, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01,
                 j_g=16, probe=48, metric="ip"),
     "tiny": dict(workload="smoke 20K x 96", n=20_000, d=96, nq=1_000, k=10, j=32, gen="latent",
                  m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=8),
