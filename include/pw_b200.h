@@ -62,8 +62,8 @@ typedef struct {
     int32_t row_copy;        /* reserved (vector rows always use cp.async; TMA measured slower) */
     int32_t flags;           /* bit 0: L2-prefetch predicted parent rows (off by default: measured slower);
                                 bit 1: lossy visited cache (ids exact, distance_computations may grow);
-                                bit 2: TMA bulk copies for expansion rows; bit 3: L2 warm-up of scoring rows
-                                (bits 0, 2, 3 are measured slower; kept for A/B) */
+                                bit 2: TMA bulk copies for expansion rows (bits 0 and 2 are measured slower;
+                                kept for A/B) */
 } pw_tuning;
 
 /* One shard (pipeline.py:121-155 build_contexts output for one ShardPack):

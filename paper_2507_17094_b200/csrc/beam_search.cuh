@@ -100,7 +100,6 @@ struct KArgs {
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
     int32_t bulk_adj;       // expansion rows 16-byte aligned: 1 cp.async x16, 2 TMA bulk (flag 4)
     int32_t prefetch;       // L2-prefetch predicted parent rows
-    int32_t warm_rows;      // L2-prefetch every row of a scoring batch beyond the first two groups
     unsigned long long* phase;  // per-phase cycle totals (PW_PHASE_TIMERS builds only)
     int32_t vis_limit;      // smem visited entries before spilling to global
     unsigned long long* gvis;  // per-warp global visited spill tables, (epoch << 32 | id)
@@ -850,26 +849,6 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             }
             cp_commit();
         };
-        // L2 warm-up two groups ahead of the staging ring (prefetch.global.L2,
-        // no staging space): group g+4 is requested while g is reduced, so its
-        // LDGSTS two steps later hits L2.  A bounded window: warming the whole
-        // batch at once overflows L2 across ~2400 resident queries (measured).
-        constexpr int LINES = (row_bytes % 128 == 0) ? row_bytes / 128 : row_bytes / 128 + 2;
-        auto warm = [&](int g) {
-            if (A.warm_rows && g < ngroups) {
-                const int r0 = g * RH;
-                const int rows = min(RH, n - r0);
-                for (int i = (int)lane; i < rows * LINES; i += 32) {
-                    const int r = i / LINES, k = i - r * LINES;
-                    const char* row = reinterpret_cast<const char*>(vrow<VT>(G, (uint32_t)S.newl[r0 + r], D));
-                    prefetch_l2(row + min(k * 128, (int)row_bytes - 4));
-                }
-            }
-        };
-        issue(0);
-        issue(1);
-        warm(2);
-        warm(3);
         const unsigned v = lane >> 2, c = lane & 3u;
         constexpr bool QREG = (D <= 128 && D % 8 == 0) || sizeof(VT) == 1;
         float2 qr[QREG ? D / 8 : 1];
@@ -878,6 +857,18 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
 #pragma unroll
             for (int p = 0; p < D / 8; p++) qr[p] = q2[4 * p + c];
         }
+        // one 8-row pass: distance -> key -> survivor compaction
+        auto emit = [&](int r0, int rows, float dist) {
+            const int rr = (int)v;
+            const int rc = rr < rows ? rr : rows - 1;
+            const uint64_t key = ((uint64_t)dist_bits<M>(dist) << 32) | (uint32_t)S.newl[r0 + rc];
+            const bool surv = c == 0 && rr < rows && key < thr;
+            const unsigned b = __ballot_sync(0xffffffffu, surv);
+            if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
+            ns += __popc(b);
+        };
+        issue(0);
+        issue(1);
         for (int g = 0; g < ngroups; g++) {
             cp_wait<1>();
             __syncwarp();
@@ -885,8 +876,7 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             const int rows = min(RH, n - r0);
             const VT* base = reinterpret_cast<const VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
             for (int pass = 0; pass < rows; pass += 8) {
-                const int rr = pass + (int)v;
-                const int rc = rr < rows ? rr : rows - 1;
+                const int rc = pass + (int)v < rows ? pass + (int)v : rows - 1;
                 float dist;
                 if constexpr (sizeof(VT) == 1)
                     dist = pw_row4_u8<M, D>(reinterpret_cast<const uint8_t*>(base + (size_t)rc * sp), qr, c);
@@ -894,15 +884,10 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
                     dist = pw_row4_qreg<M, D>(reinterpret_cast<const float*>(base + (size_t)rc * sp), qr, c);
                 else
                     dist = finish<M>(pw_sum4<M, 0, D>(reinterpret_cast<const float*>(base + (size_t)rc * sp), S.q, c));
-                const uint64_t key = ((uint64_t)dist_bits<M>(dist) << 32) | (uint32_t)S.newl[r0 + rc];
-                const bool surv = c == 0 && rr < rows && key < thr;
-                const unsigned b = __ballot_sync(0xffffffffu, surv);
-                if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
-                ns += __popc(b);
+                emit(r0 + pass, min(8, rows - pass), dist);
             }
             __syncwarp();
             issue(g + 2);
-            warm(g + 4);
         }
         cp_wait<0>();
         __syncwarp();
@@ -1621,6 +1606,13 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         }
         // query row -> smem
         for (int t = lane; t < A.d; t += 32) S.q[t] = A.queries[(size_t)row * A.d + t];
+        // the task's (qid, stage) wait in shared memory instead of registers
+        // across the search: the hot loop runs at the 128-register cap
+        int32_t* tsk = S.misc + A.o_par - 2;
+        if (lane == 0) {
+            tsk[0] = (int32_t)qid;
+            tsk[1] = stage;
+        }
         __syncwarp();
 
         int32_t g_it = 0;
@@ -1639,7 +1631,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
             bool fill_random = true;
             Pcg64 rng;
             if (gph) {
-                rng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)qid, (uint64_t)stage));
+                rng = pcg64_from_seed(derive_seed3(A.seed, 5, (uint64_t)tsk[0], (uint64_t)tsk[1]));
             } else {
                 // seeds (pipeline.py:227-231, search.py:294)
                 if (A.n_seeds > 0) {
@@ -1657,7 +1649,7 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
                 }
                 __syncwarp();
                 rng = A.rng_io ? A.rng_io[task]
-                               : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)qid, (uint64_t)stage));
+                               : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)tsk[0], (uint64_t)tsk[1]));
             }
             converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G, gph ? A.gcfg : A.cfg, ns, fill_random,
                                       rng, task, &n_logged);
@@ -1675,6 +1667,9 @@ __global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_consta
         }
 
         // outputs (search.py:323-335, pipeline.py:236-246, :339)
+        qid = tsk[0];
+        stage = tsk[1];
+        row = A.df ? qid : task;
         const uint64_t* qk = S.qk_cur();
         const int nk = min(S.qlen, A.cfg.k);
         for (int t = lane; t < nk; t += 32) {

@@ -347,8 +347,13 @@ int64_t visit_bound(const SearchCfg& c, int32_t j, int64_t n) {
     return std::min<int64_t>(b, n);
 }
 
+// st: the stream the launch will use.  Workspace (re)initialisation is
+// stream-ordered on it -- never a device-wide synchronisation, which would
+// deadlock against another shard's persistent dataflow kernel waiting for
+// this shard's entries.  A shard's searches share one stream (or are ordered
+// by the caller).
 int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_ghost_graph,
-            int32_t n_seeds, bool ghost_on, Launch& Lc) {
+            int32_t n_seeds, bool ghost_on, Launch& Lc, cudaStream_t st = 0) {
     int rc = validate_params(p);
     if (rc) return rc;
     KArgs& A = Lc.A;
@@ -473,9 +478,15 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
     A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
     A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
-    A.o_cand = (int32_t)off; off = al(off + 4 * cb);
     A.o_newl = (int32_t)off; off = al(off + 4 * cb);
-    A.o_ckey = (int32_t)off; off = al(off + 8 * std::max<int64_t>(64, next_pow2(cb)));  // pow2 for the survivor sort
+    // keys (pow2 for the survivor sort); the candidate list lives in their
+    // upper half: candidates are live from expansion to the dedup, while the
+    // key area then holds at most the DGS raw adjacency (r*j ints, lower
+    // half) and the visited probes (lower half); keys return only in scoring
+    const int64_t ckey_n = std::max<int64_t>(64, next_pow2(cb));
+    A.o_ckey = (int32_t)off;
+    A.o_cand = (int32_t)(off + 4 * ckey_n);
+    off = al(off + 8 * ckey_n);
     A.o_vh = (int32_t)off; off = al(off + 4 * H);
     A.o_stage = (int32_t)off;
     A.o_bhk = (int32_t)off;
@@ -498,9 +509,6 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
     A.bulk_rows = 0;
     A.prefetch = (tun && (tun->flags & 1)) ? 1 : 0;
-    // flag 8: L2 warm-up of scoring rows two groups ahead (opt-in: measured
-    // slower at C2 -- 4.24 -> 4.69 ms PW, 5.65 -> 5.84 ms naive)
-    A.warm_rows = (tun && (tun->flags & 8)) ? 1 : 0;
     A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
                   (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16((int64_t)elem * d) && b16(4ll * G.j * W))))
                      ? ((tun && (tun->flags & 4)) ? 2 : 1)
@@ -539,37 +547,40 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     std::lock_guard<std::mutex> lk(sh->mu);
     if (!sh->counter) {
         PW_CUDA(cudaMalloc(&sh->counter, sizeof(int32_t) * 2));
-        PW_CUDA(cudaMemset(sh->counter, 0, sizeof(int32_t) * 2));
+        PW_CUDA(cudaMemsetAsync(sh->counter, 0, sizeof(int32_t) * 2, st));
         PW_CUDA(cudaMalloc(&sh->phase, sizeof(unsigned long long) * 8));
-        PW_CUDA(cudaMemset(sh->phase, 0, sizeof(unsigned long long) * 8));
+        PW_CUDA(cudaMemsetAsync(sh->phase, 0, sizeof(unsigned long long) * 8, st));
     }
     A.phase = sh->phase;
-    if (sh->gvis_words < (size_t)total_warps * gsz || sh->gepoch_n < (size_t)total_warps) {
-        // epoch-tagged tables: zero once (epoch 0 is never used by a search)
-        if (sh->gvis) cudaFree(sh->gvis);
-        if (sh->gepoch) cudaFree(sh->gepoch);
+    const bool grow = sh->gvis_words < (size_t)total_warps * gsz || sh->gepoch_n < (size_t)total_warps;
+    const bool rezero = !grow && (sh->gvis_stride != gsz || sh->gvis_lossy != (int)lossy);
+    if (grow) {
+        // epoch-tagged tables: zero once (epoch 0 is never used by a search);
+        // stream-ordered free / alloc / zero
+        if (sh->gvis) PW_CUDA(cudaFreeAsync(sh->gvis, st));
+        if (sh->gepoch) PW_CUDA(cudaFreeAsync(sh->gepoch, st));
         sh->gvis = nullptr;
         sh->gepoch = nullptr;
         const size_t words = std::max(sh->gvis_words, (size_t)total_warps * gsz);
-        PW_CUDA(cudaMalloc(&sh->gvis, sizeof(unsigned long long) * words));
-        PW_CUDA(cudaMemset(sh->gvis, 0, sizeof(unsigned long long) * words));
-        PW_CUDA(cudaMalloc(&sh->gepoch, sizeof(uint32_t) * (size_t)total_warps));
-        PW_CUDA(cudaMemset(sh->gepoch, 0, sizeof(uint32_t) * (size_t)total_warps));
+        PW_CUDA(cudaMallocAsync((void**)&sh->gvis, sizeof(unsigned long long) * words, st));
+        PW_CUDA(cudaMemsetAsync(sh->gvis, 0, sizeof(unsigned long long) * words, st));
+        PW_CUDA(cudaMallocAsync((void**)&sh->gepoch, sizeof(uint32_t) * (size_t)total_warps, st));
+        PW_CUDA(cudaMemsetAsync(sh->gepoch, 0, sizeof(uint32_t) * (size_t)total_warps, st));
         sh->gvis_words = words;
         sh->gepoch_n = (size_t)total_warps;
         sh->gvis_stride = gsz;
-    } else if (sh->gvis_stride != gsz || sh->gvis_lossy != (int)lossy) {
+    } else if (rezero) {
         // a different per-warp stride maps regions to other warps: re-zero so no
         // stale (epoch, id) of another warp can match
-        PW_CUDA(cudaMemset(sh->gvis, 0, sizeof(unsigned long long) * sh->gvis_words));
-        PW_CUDA(cudaMemset(sh->gepoch, 0, sizeof(uint32_t) * sh->gepoch_n));
+        PW_CUDA(cudaMemsetAsync(sh->gvis, 0, sizeof(unsigned long long) * sh->gvis_words, st));
+        PW_CUDA(cudaMemsetAsync(sh->gepoch, 0, sizeof(uint32_t) * sh->gepoch_n, st));
         sh->gvis_stride = gsz;
     }
     sh->gvis_lossy = (int)lossy;
     if (sh->gscr_words < (size_t)total_warps * scr) {
-        if (sh->gscr) cudaFree(sh->gscr);
+        if (sh->gscr) PW_CUDA(cudaFreeAsync(sh->gscr, st));
         sh->gscr = nullptr;
-        PW_CUDA(cudaMalloc(&sh->gscr, sizeof(uint32_t) * (size_t)total_warps * scr));
+        PW_CUDA(cudaMallocAsync((void**)&sh->gscr, sizeof(uint32_t) * (size_t)total_warps * scr, st));
         sh->gscr_words = (size_t)total_warps * scr;
     }
     A.gvis = sh->gvis;
@@ -692,7 +703,7 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
         return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
     Launch Lc;
     bool ghost_on = params->ghost_enabled && !entries_in && sh->gn > 0;
-    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc);
+    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc, (cudaStream_t)stream);
     if (rc) return rc;
     KArgs& A = Lc.A;
     A.stage = stage;
@@ -725,7 +736,7 @@ int pw_search_dataflow(pw_shard* sh, const pw_params* params, const pw_tuning* t
     if (N > 1 && (!inbox || !next_inbox)) return set_err(PW_EINVAL, "dataflow ring needs inboxes");
     Launch Lc;
     const bool ghost_on = params->ghost_enabled && sh->gn > 0;  // stage-0 tasks only
-    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc);
+    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc, (cudaStream_t)stream);
     if (rc) return rc;
     KArgs& A = Lc.A;
     A.df = 1;

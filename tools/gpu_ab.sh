@@ -1,12 +1,15 @@
-# A/B of tools/lib_prev.so vs the working tree (CFG/L/TUNING env) after the parity tests;
-# TIMERS=1 adds the per-phase cycle breakdown, NCU=1 an ncu --set full capture of K1.
+# A/B of several libraries (LIBS, default "tools/lib_prev.so default") at CFG/L/TUNING after
+# the parity tests; TIMERS=1 adds the per-phase cycle breakdown, NCU=1 an ncu capture of K1.
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -20 gpurun_out/build.log; exit 1; }
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+if [ -z "$NOTEST" ]; then timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log; fi
 : > gpurun_out/ab.log
 for i in 1 2; do
-PW_LIB=tools/lib_prev.so timeout 900 python tools/ab.py --config ${CFG:-c2} --l ${L:-256} ${TUNING:+--tuning "$TUNING"} 2>>gpurun_out/ab.err >> gpurun_out/ab.log
-timeout 900 python tools/ab.py --config ${CFG:-c2} --l ${L:-256} ${TUNING:+--tuning "$TUNING"} 2>>gpurun_out/ab.err >> gpurun_out/ab.log
+for lib in ${LIBS:-tools/lib_prev.so default}; do
+  if [ "$lib" = default ]; then unset PW_LIB; else export PW_LIB=$lib; fi
+  timeout 900 python tools/ab.py --config ${CFG:-c2} --l ${L:-256} ${TUNING:+--tuning "$TUNING"} 2>>gpurun_out/ab.err >> gpurun_out/ab.log
 done
+done
+unset PW_LIB
 cat gpurun_out/ab.log
 if [ -n "$TIMERS" ]; then
 python -m paper_2507_17094_b200.build_ext --timers > gpurun_out/build_timers.log 2>&1
