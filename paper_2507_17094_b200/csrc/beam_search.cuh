@@ -22,7 +22,12 @@
 
 #include "rng_pcg64.cuh"
 
+#ifndef PW_MAX_THREADS
+#define PW_MAX_THREADS 512  // resident query-warps per SM x 32 (__launch_bounds__)
+#endif
+
 namespace pw {
+constexpr int kMaxWarps = PW_MAX_THREADS / 32;
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr int kMaxLeaves = 64;
@@ -1534,7 +1539,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
 }
 
 template <int D, typename VT, int M>
-__global__ void __launch_bounds__(512, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
+__global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;

@@ -463,48 +463,74 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad * elem) / per);
         PG = std::max(PG, 1);
     }
-    A.R = R;
-    A.PG = PG;
     A.pstride = pstride;
-    // The in-batch dedup hash (bhk/bhp) and its slot list (cslot) are live only
-    // between expansion and the visited filter, the staging ring only in
-    // scoring and DGS expansion (before the dedup): they share one region.
-    const int64_t hash_bytes = 8 * (int64_t)A.BH + 4 * cb;
-    const int64_t stage_bytes = std::max<int64_t>((int64_t)elem * R * spad, hash_bytes);
     // specialised kernels with j <= 32 keep the DGS counts/bits in registers
     const bool dgs_regs = specialised && G.j <= 32;
-    auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
-    int64_t off = 0;
-    A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
-    A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
-    A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
-    A.o_newl = (int32_t)off; off = al(off + 4 * cb);
-    // keys (pow2 for the survivor sort); the candidate list lives in their
-    // upper half: candidates are live from expansion to the dedup, while the
-    // key area then holds at most the DGS raw adjacency (r*j ints, lower
-    // half) and the visited probes (lower half); keys return only in scoring
-    const int64_t ckey_n = std::max<int64_t>(64, next_pow2(cb));
-    A.o_ckey = (int32_t)off;
-    A.o_cand = (int32_t)(off + 4 * ckey_n);
-    off = al(off + 8 * ckey_n);
-    A.o_vh = (int32_t)off; off = al(off + 4 * H);
-    A.o_stage = (int32_t)off;
-    A.o_bhk = (int32_t)off;
-    A.o_bhp = (int32_t)(off + 4 * (int64_t)A.BH);
-    A.o_cslot = (int32_t)(off + 8 * (int64_t)A.BH);
-    off = al(off + stage_bytes);
-    A.o_misc = (int32_t)off;
-    // misc words: [DGS counts PG*j | perm j] [DGS bits PG*W] 8 pad | parents r | 8 pad
-    const int64_t misc_cnt = dgs_regs ? (int64_t)jm : (int64_t)std::max(jm, PG * jm);
-    const int64_t misc_bits = dgs_regs ? 0 : (int64_t)PG * W;
-    A.o_par = (int32_t)(misc_cnt + misc_bits + 8);
-    int64_t misc = misc_cnt + misc_bits + 8 + p.r + 8;
-    off = al(off + 4 * misc);
-    A.o_mbar = (int32_t)off;
-    off = al(off + 3 * 8);
-    A.o_desc = (int32_t)off;
-    off = al(off + 16 * std::max<int64_t>({32, (int64_t)p.r, 3ll * PG}));  // one descriptor per fetched row
-    A.warp_bytes = (int32_t)off;
+    const int64_t n_desc = std::max<int64_t>({32, (int64_t)p.r, 3ll * kParentGroup});
+    // Per-warp shared-memory layout for R staging rows; returns bytes per warp.
+    auto layout = [&](int Rr) -> int64_t {
+        A.R = Rr;
+        // The in-batch dedup hash (bhk/bhp) and its slot list (cslot) are live
+        // only between expansion and the visited filter, the staging ring only
+        // in scoring and DGS expansion (before the dedup): they share one region.
+        const int64_t hash_bytes = 8 * (int64_t)A.BH + 4 * cb;
+        const int64_t stage_bytes = std::max<int64_t>((int64_t)elem * Rr * spad, hash_bytes);
+        if (A.cfg.prune_sel == PW_SEL_DIRECTION) {  // DGS parents per fetch round trip
+            const int64_t per = (int64_t)pstride * elem + 4ll * G.j * W;
+            PG = (int)std::max<int64_t>(1, std::min<int64_t>(kParentGroup, stage_bytes / per));
+        }
+        A.PG = PG;
+        auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
+        int64_t off = 0;
+        A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
+        A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
+        A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
+        A.o_newl = (int32_t)off; off = al(off + 4 * cb);
+        // keys (pow2 for the survivor sort); the candidate list lives in their
+        // upper half: candidates are live from expansion to the dedup, while the
+        // key area then holds at most the DGS raw adjacency (r*j ints, lower
+        // half) and the visited probes (lower half); keys return only in scoring
+        const int64_t ckey_n = std::max<int64_t>(64, next_pow2(cb));
+        A.o_ckey = (int32_t)off;
+        A.o_cand = (int32_t)(off + 4 * ckey_n);
+        off = al(off + 8 * ckey_n);
+        A.o_vh = (int32_t)off; off = al(off + 4 * H);
+        A.o_stage = (int32_t)off;
+        A.o_bhk = (int32_t)off;
+        A.o_bhp = (int32_t)(off + 4 * (int64_t)A.BH);
+        A.o_cslot = (int32_t)(off + 8 * (int64_t)A.BH);
+        off = al(off + stage_bytes);
+        A.o_misc = (int32_t)off;
+        // misc words: [DGS counts PG*j | perm j] [DGS bits PG*W] 8 pad (task
+        // scalars) | parents r | 8 pad
+        const int64_t misc_cnt = dgs_regs ? (int64_t)jm : (int64_t)std::max(jm, PG * jm);
+        const int64_t misc_bits = dgs_regs ? 0 : (int64_t)PG * W;
+        A.o_par = (int32_t)(misc_cnt + misc_bits + 8);
+        const int64_t misc = misc_cnt + misc_bits + 8 + p.r + 8;
+        off = al(off + 4 * misc);
+        A.o_mbar = (int32_t)off;
+        off = al(off + 3 * 8);
+        // expansion row descriptors live only inside one fetch, while the new-id
+        // list is dead (consumed by scoring, rewritten by the dedup)
+        if (16 * n_desc <= 4 * cb) {
+            A.o_desc = A.o_newl;
+        } else {
+            A.o_desc = (int32_t)off;
+            off = al(off + 16 * n_desc);
+        }
+        A.warp_bytes = (int32_t)off;
+        return off;
+    };
+    DevInfo* I;
+    if ((rc = dev_info(sh->device, &I))) return rc;
+    int64_t off = layout(R);
+    // kernels built for more than 16 resident warps (PW_MAX_THREADS): shrink
+    // the staging ring (down to 12 rows) until they fit
+    while (specialised && elem == 4 && !(tun && tun->stage_rows > 0) && R > 12 &&
+           I->smem_optin / off < kMaxWarps) {
+        R -= 2;
+        off = layout(R);
+    }
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
     A.bulk_rows = 0;
@@ -514,9 +540,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
                      ? ((tun && (tun->flags & 4)) ? 2 : 1)
                      : 0;
 
-    DevInfo* I;
-    if ((rc = dev_info(sh->device, &I))) return rc;
-    int wpb = (int)std::min<int64_t>(16, I->smem_optin / off);
+    int wpb = (int)std::min<int64_t>(kMaxWarps, I->smem_optin / off);
     if (tun && tun->warps_per_sm > 0) wpb = std::min(wpb, tun->warps_per_sm);
     if (wpb < 1) return set_err(PW_EINVAL, "search configuration needs " + std::to_string(off) +
                                               " bytes of shared memory per query (l or degree too large)");
