@@ -46,7 +46,7 @@ CONFIGS = {
                spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=48),
     "c1": dict(workload="SIFT-shaped 100K x 128 f32, 1K queries, k=10, degree-32 graph",
                n=100_000, d=128, nq=1_000, k=10, j=32, gen="gauss", n_clusters=8192,
-               spread=0.08, rho=0.01, j_g=16, probe=32),
+               spread=0.08, rho=0.01, j_g=16, probe=32, builder="exact"),
     "c2s": dict(workload="DEEP-shaped 1M x 96 f32 (C2 at 1/10 scale), 10K queries, k=10",
                 n=1_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
                 spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=32),
@@ -58,7 +58,7 @@ CONFIGS = {
                 dtype="u8"),
     "c4": dict(workload="GIST-shaped 1M x 960 f32, 1K queries, k=10, degree-32 graph", n=1_000_000,
                d=960, nq=1_000, k=10, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05,
-               rho=0.01, j_g=16, probe=48),
+               rho=0.01, j_g=16, probe=48, builder="exact"),
     "c5s": dict(workload="Text2Image-shaped 12.5M x 200 f32 inner product (one of C5's 8 shards of "
                          "100M), 10K queries, k=100, degree-32 graph", n=12_500_000, d=200, nq=10_000,
                 k=100, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01,
@@ -155,18 +155,38 @@ def build_workload(cfg: dict, rank: int, world: int, device):
         # unit rows (embedding-style): the L2 kNN graph ranks like inner product
         x = x / torch.linalg.vector_norm(x, dim=1, keepdim=True)
     base, queries = x[: cfg["n"]], x[cfg["n"]:].contiguous()
-    parts = builder.partition(cfg["n"], world, SEED, device=device)
-    rows = parts[rank]
-    vec = base[rows].contiguous()
+    if cfg.get("builder") == "exact":
+        # the reference's build_index semantics (graphs.py:237-299) on the
+        # GPU: partition / ghost sample from its numpy streams, exact kNN
+        # graph + reverse augmentation, exact inter-shard table and ghost graph
+        from paper_2507_17094_b200 import exact
+
+        parts = [torch.from_numpy(r).to(device) for r in exact.partition_rows(cfg["n"], world, SEED)]
+        rows = parts[rank]
+        vec = base[rows].contiguous()
+        adj = exact.build_knn_graph(vec, cfg["j"])
+        gh = None
+        if exact.ghost_count(vec.shape[0], cfg["rho"]) > cfg["j_g"]:
+            gids, gadj = exact.build_ghost_index(vec, cfg["rho"], cfg["j_g"], SEED, shard=rank)
+            gh = (torch.from_numpy(gids).to(device), gadj)
+        inter = None
+        if world > 1:
+            nxt = base[parts[(rank + 1) % world]].contiguous()
+            inter = exact.build_inter_shard_table(vec, nxt)
+            del nxt
+    else:
+        parts = builder.partition(cfg["n"], world, SEED, device=device)
+        rows = parts[rank]
+        vec = base[rows].contiguous()
+        adj = builder.knn_graph(vec, cfg["j"], probe=cfg["probe"], seed=SEED + rank)
+        gh = builder.ghost(vec, cfg["rho"], cfg["j_g"], SEED + rank)
+        inter = None
+        if world > 1:
+            nxt = base[parts[(rank + 1) % world]].contiguous()
+            inter = builder.inter_shard(vec, nxt, probe=cfg["probe"], seed=SEED + rank)
+            del nxt
     vec_dev = vec.to(torch.uint8) if cfg.get("dtype") == "u8" else vec
-    adj = builder.knn_graph(vec, cfg["j"], probe=cfg["probe"], seed=SEED + rank)
     direction = builder.direction_table(vec, adj)
-    gh = builder.ghost(vec, cfg["rho"], cfg["j_g"], SEED + rank)
-    inter = None
-    if world > 1:
-        nxt = base[parts[(rank + 1) % world]].contiguous()
-        inter = builder.inter_shard(vec, nxt, probe=cfg["probe"], seed=SEED + rank)
-        del nxt
     torch.cuda.synchronize()
     build_s = time.time() - t0
     return dict(base=base, queries=queries, rows=rows, vec=vec_dev, adj=adj, direction=direction,
@@ -380,9 +400,11 @@ def run_ours(args, cfg):
                        "index_build_s": round(W["build_s"], 1),
                        "generator": {k2: cfg[k2] for k2 in ("gen", "m", "n_clusters", "spread",
                                                             "noise") if k2 in cfg},
-                       "graph": "GPU IVF kNN (probe %d) + reverse-edge augmentation; ghost "
-                                "rho=%.2f j_g=%d; direction table" % (cfg["probe"], cfg["rho"],
-                                                                     cfg["j_g"]),
+                       "graph": ("exact kNN + reverse augmentation, exact inter-shard and ghost "
+                                 "graphs (exact.py, graphs.py semantics); rho=%.2f j_g=%d; direction "
+                                 "table" % (cfg["rho"], cfg["j_g"])) if cfg.get("builder") == "exact" else
+                                ("GPU IVF kNN (probe %d) + reverse-edge augmentation; ghost "
+                                 "rho=%.2f j_g=%d; direction table" % (cfg["probe"], cfg["rho"], cfg["j_g"])),
                        "sweep": ops["pathweaver"]["sweep"]},
             "e2e": {"value": round(nq * e2e_steps / e2e_s, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},

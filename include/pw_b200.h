@@ -190,6 +190,13 @@ int pw_search_dataflow(pw_shard* shard, const pw_params* params, const pw_tuning
                        int32_t* shard_ids, float* shard_dists, int32_t* stats_i32,
                        int64_t* stats_i64, int32_t sm_limit, void* stream);
 
+/* Exact squared L2 of row pairs for the GPU index builder (graphs.py:90-101
+ * rescoring): out[t] = squared_l2(b[ib[t]], a[ia[t]]), numpy pairwise float32
+ * order, bit-identical to data.py:70-79.  a (.., d), b (.., d) float32; ia,
+ * ib (n,) int64; out (n,) float32; device pointers, asynchronous. */
+int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, const int64_t* ib,
+                int64_t n, float* out, void* stream);
+
 /* Synchronous check of a shard's device error flag (table overflow, a
  * dataflow inbox that never filled); clears it.  0 or PW_ECUDA + message. */
 int pw_shard_check(pw_shard* shard);

@@ -87,6 +87,8 @@ EXPORTS = {
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_int32, C.c_void_p]),
     "pw_shard_check": (C.c_int, [C.c_void_p]),
+    "pw_l2_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
+                              C.c_void_p, C.c_void_p]),
     "pw_dev_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
     "pw_dev_free": (C.c_int, [C.c_void_p]),
     "pw_ipc_get": (C.c_int, [C.c_void_p, C.c_void_p]),
@@ -94,7 +96,7 @@ EXPORTS = {
     "pw_ipc_close": (C.c_int, [C.c_void_p]),
 }
 
-OPTIONAL = {"pw_phase_cycles", "pw_launch_config", "pw_search_dataflow", "pw_shard_check", "pw_dev_alloc", "pw_dev_free",
+OPTIONAL = {"pw_phase_cycles", "pw_launch_config", "pw_search_dataflow", "pw_shard_check", "pw_l2_pairs", "pw_dev_alloc", "pw_dev_free",
             "pw_ipc_get", "pw_ipc_open", "pw_ipc_close"}
 _LIB = None
 

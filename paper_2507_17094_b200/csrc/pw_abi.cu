@@ -300,6 +300,25 @@ __global__ void l2_rows_kernel(const VT* __restrict__ vec, int32_t d, int32_t sp
     }
 }
 
+// Exact squared L2 of row pairs (index builder rescoring, graphs.py:90-101,
+// :124-126): out[t] = squared_l2(b[ib[t]], a[ia[t]]) in numpy's pairwise
+// float32 order.  8 lanes per pair (the runtime pairwise plan), 4 pairs per
+// warp, rows read straight from HBM.
+__global__ void l2_pairs_kernel(const float* __restrict__ a, const float* __restrict__ b, int32_t d,
+                                L2Plan plan, const int64_t* __restrict__ ia, const int64_t* __restrict__ ib,
+                                int64_t n, float* __restrict__ out) {
+    const unsigned lane = threadIdx.x & 31u;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w * 4 < n; w += warps) {
+        const int64_t t = w * 4 + (lane >> 3);
+        const int64_t tc = t < n ? t : n - 1;
+        const float* x = b + ib[tc] * (int64_t)d;
+        const float* q = a + ia[tc] * (int64_t)d;
+        const float dist = l2_row<0, float>(plan, x, q, lane & 7u);
+        if ((lane & 7u) == 0 && t < n) out[t] = dist;
+    }
+}
+
 SearchCfg make_cfg(const pw_params& p, int64_t n, int32_t j) {
     SearchCfg c;
     c.k = p.k;
@@ -802,6 +821,20 @@ int pw_shard_check(pw_shard* sh) {
     if (!sh->counter) return 0;
     PW_CUDA(cudaSetDevice(sh->device));
     return check_err(sh);
+}
+
+int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, const int64_t* ib, int64_t n,
+                float* out, void* stream) {
+    if (n <= 0) return 0;
+    if (!a || !b || !ia || !ib || !out || d < 1) return set_err(PW_EINVAL, "bad argument");
+    L2Plan plan;
+    if (!make_plan(d, plan)) return set_err(PW_EINVAL, "dimension too large");
+    const int64_t warps = (n + 3) / 4;
+    const int blocks = (int)std::min<int64_t>(148 * 16, (warps + 7) / 8);
+    l2_pairs_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(a, b, d, plan, ia, ib, n, out);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
 }
 
 int pw_dev_alloc(int64_t bytes, void** out) {
