@@ -80,35 +80,58 @@ def log(*a):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    nvidia-smi needs a few hundred ms to start, longer than a 10-step timed
+    region, so the sampler is started first and waits for its first line; a
+    reader thread stamps every line on arrival and only lines that arrive
+    inside the timed window (padded by one period) are summarised."""
 
     FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 20
 
     def __init__(self, device_index: int):
         self.idx = device_index
         self.proc = None
+        self.lines = []
+        self.t0 = self.t1 = None
+
+    def _reader(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.perf_counter(), line))
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+        self.thread = threading.Thread(target=self._reader, daemon=True)
+        self.thread.start()
+        deadline = time.perf_counter() + 10.0
+        while not self.lines and time.perf_counter() < deadline and self.proc.poll() is None:
+            time.sleep(0.01)
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *exc):
+        self.t1 = time.perf_counter()
         if self.proc is not None:
+            time.sleep(2 * self.PERIOD_MS / 1e3)  # the sample straddling the end
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.out = out
+            self.thread.join(timeout=5)
+            pad = self.PERIOD_MS / 1e3
+            inside = [ln for t, ln in self.lines if self.t0 - pad <= t <= self.t1 + pad]
+            self.out = "".join(inside)
         return False
 
     def summary(self) -> dict:

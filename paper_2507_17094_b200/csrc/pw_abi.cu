@@ -578,7 +578,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
                        !p.log_visits;
     A.lossy = lossy ? 1 : 0;
     if (lossy) {
-        const int64_t slots = std::max<int64_t>(64, next_pow2(tun->visited_slots > 0 ? tun->visited_slots : 8192));
+        const int64_t slots = std::max<int64_t>(64, next_pow2(tun->visited_slots > 0 ? tun->visited_slots : 4096));
         int lg = 0;
         while ((1ll << lg) < slots) lg++;
         A.lshift = 32 - lg;
