@@ -66,6 +66,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     extra = ["-DPW_PHASE_TIMERS"] if timers else []
     if os.environ.get("PW_MAX_THREADS"):  # A/B builds with more resident warps per SM
         extra.append(f"-DPW_MAX_THREADS={int(os.environ['PW_MAX_THREADS'])}")
+    extra += os.environ.get("PW_EXTRA_NVCC", "").split()  # A/B build variants (-DPW_...)
     jobs_list = [([nv, *CFLAGS, *extra, "-c", str(CSRC / "pw_abi.cu"), "-o", str(bdir / "pw_abi.o")],
                   bdir / "pw_abi.o")]
     for d in DIMS:

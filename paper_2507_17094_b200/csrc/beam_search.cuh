@@ -161,6 +161,27 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+#ifndef PW_EVICT_FIRST
+#define PW_EVICT_FIRST 0
+#endif
+// Streaming rows (vectors, adjacency, direction: no reuse across queries)
+// optionally carry an L2 evict-first hint so they do not push the lossy
+// visited caches and the ghost graph out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol = 0;
+#if PW_EVICT_FIRST
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
+}
+__device__ __forceinline__ void cp_async16_stream(uint32_t s, const void* gmem, uint64_t pol) {
+#if PW_EVICT_FIRST
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
+#else
+    (void)pol;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+#endif
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -833,6 +854,7 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
     if constexpr (D > 0) {
         constexpr uint32_t row_bytes = D * (uint32_t)sizeof(VT);
         constexpr int CPR = row_bytes / 16;  // 16-byte chunks per row
+        const uint64_t pol = l2_evict_first_policy();
         auto issue = [&](int g) {
             if (g < ngroups) {
                 const int r0 = g * RH;
@@ -849,7 +871,9 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
 #pragma unroll
                     for (int k = 0; k < CPL; k++) {
                         const int ch = sub + k * LPR;
-                        if (CPR % LPR == 0 || ch < CPR) cp_async16(dst + (16 / sizeof(VT)) * ch, src + (16 / sizeof(VT)) * ch);
+                        if (CPR % LPR == 0 || ch < CPR)
+                            cp_async16_stream((uint32_t)__cvta_generic_to_shared(dst + (16 / sizeof(VT)) * ch),
+                                              src + (16 / sizeof(VT)) * ch, pol);
                     }
                 }
             }
@@ -1157,12 +1181,12 @@ static __device__ __noinline__ uint32_t bulk_issue_wait(const uint4* desc, uint6
 static __device__ __forceinline__ void copy16_issue_wait(const uint4* desc, int n_rows) {
     const unsigned lane = lane_id();
     const unsigned sub = lane & 7u;
+    const uint64_t pol = l2_evict_first_policy();
     for (int r = (int)(lane >> 3); r < n_rows; r += 4) {
         const uint4 d = desc[r];
         const char* src = reinterpret_cast<const char*>(((uint64_t)d.w << 32) | d.z);
         const uint32_t nch = d.y >> 4;
-        for (uint32_t c = sub; c < nch; c += 8)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d.x + 16 * c), "l"(src + 16 * c));
+        for (uint32_t c = sub; c < nch; c += 8) cp_async16_stream(d.x + 16 * c, src + 16 * c, pol);
     }
     cp_commit();
     cp_wait<0>();
