@@ -162,11 +162,12 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 #ifndef PW_EVICT_FIRST
-#define PW_EVICT_FIRST 0
+#define PW_EVICT_FIRST 1
 #endif
 // Streaming rows (vectors, adjacency, direction: no reuse across queries)
-// optionally carry an L2 evict-first hint so they do not push the lossy
-// visited caches and the ghost graph out of L2.
+// carry an L2 evict-first hint so they do not push the lossy visited caches
+// and the ghost graph out of L2 (C2: naive 5.36 -> 4.80 ms, PW 4.21 -> 4.05 ms;
+// -DPW_EVICT_FIRST=0 builds without).
 __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     uint64_t pol = 0;
 #if PW_EVICT_FIRST
