@@ -175,6 +175,35 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 #endif
     return pol;
 }
+#ifndef PW_EVICT_LAST
+#define PW_EVICT_LAST 0
+#endif
+// Reused data -- the lossy visited caches and the ghost graph (every query's
+// stage-0 search walks it) -- optionally ask L2 to keep it (evict-last).
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol = 0;
+#if PW_EVICT_LAST
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
+}
+__device__ __forceinline__ void cp_async4_keep(void* smem, const void* gmem, uint64_t pol) {
+#if PW_EVICT_LAST
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem), "l"(pol));
+#else
+    (void)pol;
+    cp_async4(smem, gmem);
+#endif
+}
+__device__ __forceinline__ void st_keep(uint32_t* p, uint32_t v, uint64_t pol) {
+#if PW_EVICT_LAST
+    asm volatile("st.global.cg.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#else
+    (void)pol;
+    __stcg(p, v);
+#endif
+}
 __device__ __forceinline__ void cp_async16_stream(uint32_t s, const void* gmem, uint64_t pol) {
 #if PW_EVICT_FIRST
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
@@ -736,7 +765,8 @@ static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S
     uint32_t* vs = reinterpret_cast<uint32_t*>(S.ckey);
     const uint32_t tag = S.epoch << 24;
 #pragma unroll 1
-    for (int t = lane; t < nb; t += 32) cp_async4(vs + t, tab + (hash32((uint32_t)S.newl[t]) >> A.lshift));
+    const uint64_t keep = l2_evict_last_policy();
+    for (int t = lane; t < nb; t += 32) cp_async4_keep(vs + t, tab + (hash32((uint32_t)S.newl[t]) >> A.lshift), keep);
     cp_commit();
     cp_wait<0>();
     __syncwarp();
@@ -746,7 +776,7 @@ static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S
         const int t = base + (int)lane;
         const uint32_t id = t < nb ? (uint32_t)S.newl[t] : 0u;
         const bool fresh = t < nb && vs[t] != (tag | id);
-        if (fresh) __stcg(&tab[hash32(id) >> A.lshift], tag | id);
+        if (fresh) st_keep(&tab[hash32(id) >> A.lshift], tag | id, keep);
         const unsigned b = __ballot_sync(0xffffffffu, fresh);
         if (fresh) S.newl[cnt + __popc(b & lanemask_lt())] = (int32_t)id;
         cnt += __popc(b);
@@ -855,7 +885,9 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
     if constexpr (D > 0) {
         constexpr uint32_t row_bytes = D * (uint32_t)sizeof(VT);
         constexpr int CPR = row_bytes / 16;  // 16-byte chunks per row
-        const uint64_t pol = l2_evict_first_policy();
+        // the ghost graph's rows are reused by every query: not streaming
+        const uint64_t pol = (PW_EVICT_LAST && G.vec == A.ghost.vec) ? l2_evict_last_policy()
+                                                                     : l2_evict_first_policy();
         auto issue = [&](int g) {
             if (g < ngroups) {
                 const int r0 = g * RH;
