@@ -62,6 +62,21 @@ def run_ring_pipelined(stage_fn, q: int, rank: int, world: int, send_recv) -> No
             send_recv(fwd, lo[cn], lo[cn + 1] - lo[cn])
 
 
+def dataflow_tasks(rank: int, world: int, q: int) -> list[tuple[int, int]]:
+    """The (stage, query) task list of one shard in the dataflow ring, in the
+    order the persistent kernel takes them (pw_search_dataflow: df_base /
+    df_lo): stage-major, stage s covering chunk (rank - s) mod N in query
+    order.  Stage-0 tasks need no input; a stage-s task's entry comes from
+    the previous shard's stage s-1 task of the same query, which that shard
+    takes earlier in its own stage-major order -- so waits never form a cycle."""
+    lo = chunk_bounds(q, world)
+    out = []
+    for stage in range(world):
+        c = ring_schedule(rank, world, stage)
+        out += [(stage, qid) for qid in range(lo[c], lo[c + 1])]
+    return out
+
+
 class RingSearch:
     """Device engine of one rank (one shard on this GPU)."""
 
