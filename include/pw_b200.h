@@ -226,6 +226,21 @@ int pw_launch_config(pw_shard* shard, const pw_params* params, const pw_tuning* 
  * PW_PHASE_TIMERS build (libpwb200_timers.so, tools/phase_timers.py). */
 int pw_phase_cycles(pw_shard* shard, int64_t* out8, int32_t reset);
 
+/* CRC-32C (Castagnoli, reflected 0x82F63B78; init ~0, final ~) for the
+ * `.pwix` index container.
+ * pw_crc32c          replaces shardann/_crc32c.py:98-130 crc32c on a HOST
+ *                    buffer: SSE4.2 crc32 instruction, split over `threads`
+ *                    host threads (<= 0: all cores) and combined.
+ * pw_crc32c_combine  replaces shardann/_crc32c.py:85-89 crc32c_combine.
+ * pw_crc32c_device   the section checks of shardann/container.py:117-124
+ *                    (_read_array) on DEVICE buffers already in HBM: n
+ *                    buffers, one K3 launch on `stream`, synchronous, CRCs
+ *                    written to out_host[n]. */
+int pw_crc32c(const void* buf, int64_t n, int32_t threads, uint32_t* out);
+int pw_crc32c_combine(uint32_t crc1, uint32_t crc2, int64_t len2, uint32_t* out);
+int pw_crc32c_device(const void* const* ptrs, const int64_t* lens, int32_t n, uint32_t* out_host,
+                     void* stream);
+
 /* Number of kernel launches issued by this library since load (evidence for
  * bench.py's gpu_launches). */
 int64_t pw_launch_count(void);

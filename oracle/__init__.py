@@ -106,6 +106,8 @@ def lib():
                                       C.POINTER(_Pcg), C.POINTER(C.c_int32), C.POINTER(_Counters)]
         L.orc_run.argtypes = [C.POINTER(_Shard), C.c_int32, C.c_void_p, C.c_int64,
                               C.POINTER(_Params), C.c_int32, C.c_int32] + [C.c_void_p] * 7
+        L.orc_crc32c_update.restype = C.c_uint32
+        L.orc_crc32c_update.argtypes = [C.c_uint32, C.c_void_p, C.c_int64]
         L.orc_reduce_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                       C.c_void_p, C.c_void_p]
         L.orc_run_stage.argtypes = [C.POINTER(_Shard), C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
@@ -310,6 +312,14 @@ def run(queries: np.ndarray, contexts, params, mode: str, threads: int = 0) -> d
         stages.append(st)
     return dict(shard_ids=shard_ids, shard_dists=shard_dists, final_ids=final_ids,
                 final_dists=final_dists, stages=stages, comm_stage_bytes=comm)
+
+
+def crc32c(data) -> int:
+    """_crc32c.py:98-130 crc32c (serial definition, _crc32c.py:17-37)."""
+    buf = np.ascontiguousarray(np.frombuffer(data, np.uint8) if isinstance(data, (bytes, bytearray))
+                               else np.asarray(data).view(np.uint8).ravel())
+    raw = lib().orc_crc32c_update(0xFFFFFFFF, buf.ctypes.data if buf.size else None, buf.size)
+    return (~raw) & 0xFFFFFFFF
 
 
 def reduce_topk(ids, dists, k: int):

@@ -812,3 +812,24 @@ int orc_run(const orc_shard* shards, int32_t n_shards, const float* queries, int
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------ CRC-32C
+ * _crc32c.py:17-29 _make_tables (table 0: eight reflected shifts of the byte
+ * by polynomial 0x82F63B78) and :32-37 _update_serial (one table step per
+ * byte).  The reference's lane/GF(2)-stitch path for large buffers
+ * (_crc32c.py:98-130) computes the same function; this restatement keeps the
+ * plain serial definition so it checks both. */
+uint32_t orc_crc32c_update(uint32_t state, const uint8_t* buf, int64_t n) {
+    static uint32_t tab[256];
+    static int ready = 0;
+    if (!ready) {
+        for (uint32_t i = 0; i < 256; ++i) {
+            uint32_t c = i;
+            for (int b = 0; b < 8; ++b) c = (c & 1u) ? (c >> 1) ^ 0x82F63B78u : c >> 1;
+            tab[i] = c;
+        }
+        ready = 1;
+    }
+    for (int64_t i = 0; i < n; ++i) state = (state >> 8) ^ tab[(state ^ buf[i]) & 0xFFu];
+    return state;
+}

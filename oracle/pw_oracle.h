@@ -129,6 +129,11 @@ int orc_run_stage(const orc_shard* shard, const float* queries, int64_t q_total,
 int orc_reduce_topk(const int32_t* ids, const float* dists, int64_t n, int32_t k,
                     int32_t* out_ids, float* out_dists);
 
+/* _crc32c.py:17-39: CRC-32C, byte-table serial path (_make_tables table 0 +
+ * _update_serial), starting from raw register `state`; crc32c(buf) =
+ * ~orc_crc32c_update(0xFFFFFFFF, buf, n). */
+uint32_t orc_crc32c_update(uint32_t state, const uint8_t* buf, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,20 @@ behaviour, computed by hand-written sm_100a CUDA kernels behind the C ABI in
 compute entry point raises when the CUDA library or device is missing.
 """
 
+from .container import (
+    ChecksumError,
+    DeviceIndex,
+    IndexFormatError,
+    VersionError,
+    crc32c,
+    crc32c_combine,
+    crc32c_device,
+    deserialize_index,
+    index_equal,
+    index_file_checksum,
+    load_index_device,
+    serialize_index,
+)
 from .data import DataFormatError, Dataset
 from .graphs import Index, ShardPack, words_per_vector
 from .pipeline import (

@@ -94,6 +94,9 @@ EXPORTS = {
     "pw_ipc_get": (C.c_int, [C.c_void_p, C.c_void_p]),
     "pw_ipc_open": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     "pw_ipc_close": (C.c_int, [C.c_void_p]),
+    "pw_crc32c": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_uint32)]),
+    "pw_crc32c_combine": (C.c_int, [C.c_uint32, C.c_uint32, C.c_int64, C.POINTER(C.c_uint32)]),
+    "pw_crc32c_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
 }
 
 OPTIONAL = {"pw_phase_cycles", "pw_launch_config", "pw_search_dataflow", "pw_shard_check", "pw_l2_pairs", "pw_dev_alloc", "pw_dev_free",

@@ -68,7 +68,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
         extra.append(f"-DPW_MAX_THREADS={int(os.environ['PW_MAX_THREADS'])}")
     extra += os.environ.get("PW_EXTRA_NVCC", "").split()  # A/B build variants (-DPW_...)
     jobs_list = [([nv, *CFLAGS, *extra, "-c", str(CSRC / "pw_abi.cu"), "-o", str(bdir / "pw_abi.o")],
-                  bdir / "pw_abi.o")]
+                  bdir / "pw_abi.o"),
+                 ([nv, *CFLAGS, *extra, "-c", str(CSRC / "pw_crc32c.cu"), "-o", str(bdir / "pw_crc32c.o")],
+                  bdir / "pw_crc32c.o")]
     for d in DIMS:
         obj = bdir / f"k_{d}.o"
         jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",

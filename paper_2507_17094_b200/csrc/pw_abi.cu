@@ -662,6 +662,10 @@ int launch(pw_shard* sh, Launch& Lc, cudaStream_t st) {
 
 }  // namespace
 
+// shared with the other translation units of libpwb200.so (pw_crc32c.cu)
+int pw_internal_set_err(int code, const char* msg) { return set_err(code, msg); }
+void pw_internal_count_launch() { g_launches++; }
+
 extern "C" {
 
 const char* pw_last_error(void) { return g_err.c_str(); }
