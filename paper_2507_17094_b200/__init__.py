@@ -21,7 +21,16 @@ from .container import (
     load_index_device,
     serialize_index,
 )
-from .data import DataFormatError, Dataset
+from .data import (
+    DataFormatError,
+    Dataset,
+    file_size_for,
+    load_fvecs,
+    load_fvecs_device,
+    load_ivecs,
+    save_fvecs,
+    save_ivecs,
+)
 from .graphs import Index, ShardPack, words_per_vector
 from .pipeline import (
     NeighborList,
@@ -33,6 +42,18 @@ from .pipeline import (
     run_ghost_stage,
     run_pipelined,
     run_sharded_baseline,
+)
+from .metrics import (
+    RunMetrics,
+    classify_visits,
+    collect_metrics,
+    cost_model_report,
+    mean_recall,
+    read_sweep_csv,
+    recall_at_k,
+    sweep,
+    write_metrics_json,
+    write_sweep_csv,
 )
 from .search import (
     DeviceShard,

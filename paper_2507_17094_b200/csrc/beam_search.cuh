@@ -204,8 +204,17 @@ __device__ __forceinline__ void st_keep(uint32_t* p, uint32_t v, uint64_t pol) {
     __stcg(p, v);
 #endif
 }
+// HINT = false for the uint8-row instances: with the hint, ptxas 12.9 emits
+// LDGSTS with an odd uniform descriptor register (desc[UR1]) there, which
+// faults as an illegal instruction (tests/test_abi.py guards the SASS).
+template <bool HINT = true>
 __device__ __forceinline__ void cp_async16_stream(uint32_t s, const void* gmem, uint64_t pol) {
 #if PW_EVICT_FIRST
+    if constexpr (!HINT) {
+        (void)pol;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+        return;
+    }
     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol));
 #else
     (void)pol;
@@ -905,7 +914,7 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
                     for (int k = 0; k < CPL; k++) {
                         const int ch = sub + k * LPR;
                         if (CPR % LPR == 0 || ch < CPR)
-                            cp_async16_stream((uint32_t)__cvta_generic_to_shared(dst + (16 / sizeof(VT)) * ch),
+                            cp_async16_stream<sizeof(VT) != 1>((uint32_t)__cvta_generic_to_shared(dst + (16 / sizeof(VT)) * ch),
                                               src + (16 / sizeof(VT)) * ch, pol);
                     }
                 }

@@ -82,3 +82,21 @@ def test_no_fused_multiply_add_in_distance_code():
     sass = subprocess.run([tool, "-sass", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
     assert "beam_search_kernel" in sass
     assert "FFMA2" not in sass
+
+
+def test_no_odd_uniform_memory_descriptors():
+    """Memory descriptors are 64-bit uniform register pairs.  ptxas 12.9 once
+    emitted `LDGSTS ... desc[UR1]` for the uint8-row K1 instances with an L2
+    cache-hint copy, which faults at run time as an illegal instruction; the
+    library must contain no odd descriptor register."""
+    import shutil
+    import subprocess
+
+    from paper_2507_17094_b200 import _abi
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(tool).exists():
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", str(_abi.LIB_PATH)], capture_output=True, text=True).stdout
+    odd = sorted(set(re.findall(r"desc\[UR\d*[13579]\]", sass)))
+    assert not odd, odd
