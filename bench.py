@@ -375,7 +375,10 @@ def run_ours(args, cfg):
     dc_per_q = float(sum(s["distance_computations"].sum() for s in stats)) / nq
 
     # ---- e2e through the C ABI with host buffers (N=1: pw_run; N>1: ring with host I/O)
-    qhost = queries.cpu().numpy()
+    # host queries in page-locked memory (the e2e contract's pinned inputs)
+    qhost = torch.empty(tuple(queries.shape), dtype=queries.dtype, pin_memory=True)
+    qhost.copy_(queries.cpu())
+    qhost = qhost.numpy()
     e2e_steps = max(3, args.steps)
     for _ in range(2):
         eng.run_host(qhost, pw_params)
