@@ -17,7 +17,7 @@ for r in csv.DictReader(lines):
     if r["Metric Name"] != "gpu__time_duration.sum":
         continue
     name = r["Kernel Name"]
-    if not any(o in name for o in OURS):
+    if not any(o in name for o in OURS) or any(x in name for x in ("native::", "at::", "at_cuda_detail")):
         continue
     scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(r["Metric Unit"], 1e-6)
     rows.append((name.split("(")[0], float(r["Metric Value"].replace(",", "")) * scale))
