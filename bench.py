@@ -224,20 +224,24 @@ def ground_truth(W: dict, k: int, metric: str = "l2") -> np.ndarray:
     return builder.exact_knn_rescored(W["base"], W["queries"], k).cpu().numpy()
 
 
-# PathWeaver's own knob: the DGS discard ratio is searched with l (both are
-# parameters of the arm; the naive arm has only l).  Measured at C2 (K1 ms at
-# the first l reaching recall 0.95, tools/explore_params.py): 0.5 4.08,
-# 0.6 3.87, 0.7 3.60, 0.75 3.47, 0.8 3.41, 0.85 3.71 (l=288), 0.9 6.35 (l=384).
-PW_DISCARDS = (0.5, 0.6, 0.7, 0.75, 0.8)
+# PathWeaver's own knobs -- the DGS discard ratio and the ghost search's
+# iteration budget -- are searched with l (all are parameters of the arm; the
+# naive arm has only l).  Measured at C2 (K1 ms at the first l reaching recall
+# 0.95, tools/explore_params.py / explore_variants.py): discard 0.5 4.08,
+# 0.6 3.87, 0.7 3.60, 0.75 3.47, 0.8 3.41, 0.85 3.71 (l=288), 0.9 6.35
+# (l=384); at discard 0.8: ghost_max_iter 16 3.98, 8 3.40, 4 3.04 (no ghost
+# stage at all: 2.72 -- an ablation, not the PathWeaver arm); m 32/64/128 and
+# r 6/10 no better than m=64, r=8.
+PW_GRID = tuple((dr, gi) for dr in (0.5, 0.7, 0.8) for gi in (8, 4, 2, 1))
 
 
-def arm_params(kind: str, l: int, k: int, metric: str = "l2", discard: float = 0.5):
+def arm_params(kind: str, l: int, k: int, metric: str = "l2", discard: float = 0.5, ghost_iter: int = 8):
     from paper_2507_17094_b200 import SearchParams
 
     if kind == "pathweaver":  # PPE + ghost staging + direction-guided selection
         return SearchParams(k=k, l=l, m=64, r=8, max_iter=64, seed=SEED % 1000,
                             selection="direction", discard_ratio=discard, cooldown_ratio=0.3,
-                            ghost_enabled=True, ghost_max_iter=8, metric=metric)
+                            ghost_enabled=True, ghost_max_iter=ghost_iter, metric=metric)
     return SearchParams(k=k, l=l, m=64, r=8, max_iter=64, seed=SEED % 1000, metric=metric)  # naive
 
 
@@ -315,13 +319,13 @@ def run_ours(args, cfg):
     ops = {}
     for kind, mode in (("pathweaver", "pipelined"), ("naive", "baseline")):
         cands = []
-        for dr in (PW_DISCARDS if kind == "pathweaver" else (0.5,)):
+        for dr, gi in (PW_GRID if kind == "pathweaver" else ((0.5, 8),)):
             chosen = None
             sweep = []
             for l in L_GRID:
                 if l < k:
                     continue
-                p = arm_params(kind, l, k, metric, dr)
+                p = arm_params(kind, l, k, metric, dr, gi)
                 ids = search(p, mode)
                 # the metric is recall@10 (for k = 100 lists: their first 10 vs the true top 10)
                 rec = builder.recall_at_k(ids, truth, RECALL_AT) if rank == 0 else 0.0
@@ -335,17 +339,18 @@ def run_ours(args, cfg):
                     break
             if chosen is None:
                 chosen = (sweep[-1][0], sweep[-1][1])
-            ms = quick_ms(arm_params(kind, chosen[0], k, metric, dr), mode) if kind == "pathweaver" else 0.0
-            cands.append(dict(l=chosen[0], recall=chosen[1], sweep=sweep, mode=mode, discard=dr,
+            ms = quick_ms(arm_params(kind, chosen[0], k, metric, dr, gi), mode) if kind == "pathweaver" else 0.0
+            cands.append(dict(l=chosen[0], recall=chosen[1], sweep=sweep, mode=mode, discard=dr, ghost_iter=gi,
                               quick_ms=round(ms, 3), ok=chosen[1] >= 0.95))
-            log(f"[rank {rank}] {kind} discard {dr}: sweep {sweep} -> l={chosen[0]} ({ms:.3f} ms)")
+            log(f"[rank {rank}] {kind} discard {dr} ghost_max_iter {gi}: sweep {sweep} -> l={chosen[0]}"
+                f" ({ms:.3f} ms)")
         ok = [c for c in cands if c["ok"]] or cands
         best = min(ok, key=lambda c: c["quick_ms"])
-        best["grid"] = [(c["discard"], c["l"], round(c["recall"], 4), c["quick_ms"]) for c in cands]
+        best["grid"] = [(c["discard"], c["ghost_iter"], c["l"], round(c["recall"], 4), c["quick_ms"]) for c in cands]
         ops[kind] = best
 
     def timed(kind, steps, warmup, with_timer=False):
-        p = arm_params(kind, ops[kind]["l"], k, metric, ops[kind]["discard"])
+        p = arm_params(kind, ops[kind]["l"], k, metric, ops[kind]["discard"], ops[kind]["ghost_iter"])
         mode = ops[kind]["mode"]
         for _ in range(warmup):
             search(p, mode)
@@ -384,7 +389,8 @@ def run_ours(args, cfg):
     # (tuning flag 2) the timed run re-scores a few forgotten nodes, so the
     # counters come from one exact-visited run (identical ids and counters
     # except distance_computations).
-    pw_params = arm_params("pathweaver", ops["pathweaver"]["l"], k, metric, ops["pathweaver"]["discard"])
+    pw_params = arm_params("pathweaver", ops["pathweaver"]["l"], k, metric, ops["pathweaver"]["discard"],
+                           ops["pathweaver"]["ghost_iter"])
     search(pw_params, "pipelined")
     dc_gathered = float(sum(s["distance_computations"].sum() for s in eng.last_stats())) / nq
     exact_tuning = dict(tuning or {})
@@ -449,9 +455,12 @@ def run_ours(args, cfg):
                        "ring": ("dataflow (P2P inbox stores)" if use_df else "stage (NCCL P2P)")
                        if world > 1 else None,
                        "arm": "pipelined path extension + ghost staging (rho=0.01) + direction-guided"
-                              " selection (discard %.2f, cooldown 0.3)" % ops["pathweaver"]["discard"],
+                              " selection (discard %.2f, cooldown 0.3), ghost_max_iter %d" % (
+                                  ops["pathweaver"]["discard"], ops["pathweaver"]["ghost_iter"]),
                        "dgs_discard": ops["pathweaver"]["discard"],
-                       "dgs_grid": ops["pathweaver"]["grid"],
+                       "ghost_max_iter": ops["pathweaver"]["ghost_iter"],
+                       "pw_grid": {"columns": ["discard", "ghost_max_iter", "l", "recall", "ms"],
+                                   "rows": ops["pathweaver"]["grid"]},
                        "l": ops["pathweaver"]["l"], "recall_at_10": ops["pathweaver"]["recall"],
                        "m": 64, "r": 8, "max_iter": 64, "tuning": tuning,
                        "l2_policy": "inputs larger than L2 (vectors %.2f GB + graph/direction %.2f GB "
@@ -472,7 +481,8 @@ def run_ours(args, cfg):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic_for(cfg, ops["pathweaver"]["l"], ops["pathweaver"]["discard"]),
+                         "traffic": traffic_for(cfg, ops["pathweaver"]["l"], ops["pathweaver"]["discard"],
+                                               ops["pathweaver"]["ghost_iter"]),
                          "kernel": "beam_search_kernel",
                          "algorithmic_bytes_per_step": int(bytes_step),
                          "kernel_ms_per_step": round(kern_ms / args.steps, 4),
@@ -494,7 +504,7 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
-def traffic_for(cfg: dict, l: int, discard: float = 0.5):
+def traffic_for(cfg: dict, l: int, discard: float = 0.5, ghost_iter: int = 8):
     """DRAM bytes (read + write) per K1 launch from the latest committed ncu
     --set full capture of the same workload/operating point, else None."""
     for path in sorted((ROOT / "profiles").glob("r*/k1_traffic.json"), reverse=True):
@@ -504,7 +514,8 @@ def traffic_for(cfg: dict, l: int, discard: float = 0.5):
             continue
         for t in entries if isinstance(entries, list) else [entries]:
             if t.get("workload") == cfg["workload"] and t.get("l") == l and \
-                    float(t.get("dgs_discard", 0.5)) == float(discard):
+                    float(t.get("dgs_discard", 0.5)) == float(discard) and \
+                    int(t.get("ghost_max_iter", 8)) == int(ghost_iter):
                 return int(t["traffic_bytes_per_launch"])
     return None
 
@@ -578,11 +589,11 @@ def run_reference(args, cfg):
     # l reaching recall 0.95, then the (discard, l) pair with the best QPS
     n = min(qh.shape[0], 2000)
     cands = []
-    for dr in PW_DISCARDS:
+    for dr, gi in PW_GRID:
         chosen = None
         sweep = []
         for l in L_GRID:
-            p = arm_params("pathweaver", l, k, metric, dr)
+            p = arm_params("pathweaver", l, k, metric, dr, gi)
             res = oracle.run(qh, [ctx], p, "pipelined", threads=threads)
             rec = builder.recall_at_k(res["final_ids"], truth, RECALL_AT)
             sweep.append((l, round(rec, 4)))
@@ -591,14 +602,14 @@ def run_reference(args, cfg):
                 break
         ok = chosen is not None
         chosen = chosen or sweep[-1][0]
-        p = arm_params("pathweaver", chosen, k, metric, dr)
+        p = arm_params("pathweaver", chosen, k, metric, dr, gi)
         t0 = time.perf_counter()
         oracle.run(qh[:n], [ctx], p, "pipelined", threads=threads)
-        cands.append(dict(discard=dr, l=chosen, sweep=sweep, ok=ok, s=time.perf_counter() - t0))
+        cands.append(dict(discard=dr, ghost_iter=gi, l=chosen, sweep=sweep, ok=ok, s=time.perf_counter() - t0))
     pool = [c for c in cands if c["ok"]] or cands
     best = min(pool, key=lambda c: c["s"])
     chosen, sweep = best["l"], best["sweep"]
-    p = arm_params("pathweaver", chosen, k, metric, best["discard"])
+    p = arm_params("pathweaver", chosen, k, metric, best["discard"], best["ghost_iter"])
     for _ in range(args.warmup):
         oracle.run(qh[:n], [ctx], p, "pipelined", threads=threads)
     t0 = time.perf_counter()
@@ -612,8 +623,10 @@ def run_reference(args, cfg):
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": cfg.get("dtype", "f32"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "l": chosen, "sweep": sweep, "shards": 1,
-                   "metric": metric, "dgs_discard": best["discard"],
-                   "dgs_grid": [(c["discard"], c["l"], c["sweep"][-1][1], round(c["s"], 3)) for c in cands]},
+                   "metric": metric, "dgs_discard": best["discard"], "ghost_max_iter": best["ghost_iter"],
+                   "pw_grid": {"columns": ["discard", "ghost_max_iter", "l", "recall", "sample_s"],
+                               "rows": [(c["discard"], c["ghost_iter"], c["l"], c["sweep"][-1][1],
+                                         round(c["s"], 3)) for c in cands]}},
         "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{n} of {qh.shape[0]} queries per step (oracle/pw_oracle.c,"

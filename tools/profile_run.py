@@ -23,13 +23,14 @@ ap.add_argument("--l", type=int, default=160)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--tuning", default="")
 ap.add_argument("--discard", type=float, default=0.5)
+ap.add_argument("--ghost-iter", type=int, default=8)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 W = bench.build_workload(cfg, 0, 1, torch.device("cuda", 0))
 gh = W["ghost"] or (None, None)
 shard = dv.TensorShard(W["vec"], W["adj"], W["rows"].to(torch.int32), W["direction"], None, gh[0], gh[1])
 run = dv.DeviceRun(W["queries"].shape[0], 1, cfg["k"], "cuda")
-p = bench.arm_params(args.arm, args.l, cfg["k"], discard=args.discard)
+p = bench.arm_params(args.arm, args.l, cfg["k"], discard=args.discard, ghost_iter=args.ghost_iter)
 mode = "pipelined" if args.arm == "pathweaver" else "baseline"
 import json
 tuning = json.loads(args.tuning) if args.tuning else None
