@@ -651,10 +651,21 @@ int launch(pw_shard* sh, Launch& Lc, cudaStream_t st) {
     if (Lc.A.n_tasks <= 0) return 0;
     PW_CUDA(cudaSetDevice(sh->device));
     PW_CUDA(cudaMemsetAsync(sh->counter, 0, sizeof(int32_t), st));  // task counter only; err sticks
-    int blocks = std::min<int64_t>(Lc.blocks, ((int64_t)Lc.A.n_tasks + Lc.warps_per_block - 1) / Lc.warps_per_block);
+    // Small batches (fewer tasks than resident query-warps, e.g. 1K GIST
+    // queries or one ring chunk) are spread over every SM with fewer warps per
+    // CTA instead of packing 16 warps into the first SMs: each query then
+    // shares its SM's issue slots and L1 with fewer others.  K1 indexes its
+    // per-warp workspace by blockIdx * (blockDim / 32) + warp, a subset of
+    // the prepared blocks x warps_per_block.
+    int wpb = Lc.warps_per_block;
+    int64_t blocks = Lc.blocks;
+    if (blocks * wpb > (int64_t)Lc.A.n_tasks) {
+        wpb = (int)std::min<int64_t>(wpb, std::max<int64_t>(1, (Lc.A.n_tasks + blocks - 1) / blocks));
+        blocks = std::min<int64_t>(blocks, ((int64_t)Lc.A.n_tasks + wpb - 1) / wpb);
+    }
+    const size_t smem = Lc.smem / (size_t)Lc.warps_per_block * (size_t)wpb;
     void* args[] = {(void*)&Lc.A};
-    PW_CUDA(cudaLaunchKernel((const void*)Lc.fn, dim3(blocks), dim3(32 * Lc.warps_per_block), args,
-                             Lc.smem, st));
+    PW_CUDA(cudaLaunchKernel((const void*)Lc.fn, dim3((unsigned)blocks), dim3(32 * wpb), args, smem, st));
     g_launches++;
     PW_CUDA(cudaGetLastError());
     return 0;
