@@ -372,7 +372,7 @@ int64_t visit_bound(const SearchCfg& c, int32_t j, int64_t n) {
 // this shard's entries.  A shard's searches share one stream (or are ordered
 // by the caller).
 int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_ghost_graph,
-            int32_t n_seeds, bool ghost_on, Launch& Lc, cudaStream_t st = 0) {
+            int32_t n_seeds, bool ghost_on, Launch& Lc, cudaStream_t st = 0, int64_t n_tasks_hint = 0) {
     int rc = validate_params(p);
     if (rc) return rc;
     KArgs& A = Lc.A;
@@ -548,6 +548,18 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     while (specialised && elem == 4 && !(tun && tun->stage_rows > 0) && R > 12 &&
            I->smem_optin / off < kMaxWarps) {
         R -= 2;
+        off = layout(R);
+    }
+    // Small batches need fewer resident query-warps per SM (launch() spreads
+    // them over every SM), so the staging ring may take the shared memory the
+    // absent warps would have used: more rows per compute pass.  This is what
+    // large rows need most (d=960: 2 rows at full occupancy, one row per
+    // 8-row pass).
+    if (n_tasks_hint > 0 && specialised && elem == 4 && !(tun && tun->stage_rows > 0)) {
+        const int64_t need = std::min<int64_t>(kMaxWarps, (n_tasks_hint + I->sms - 1) / I->sms);
+        int Rb = R;
+        while (Rb + 2 <= 16 && layout(Rb + 2) * need <= I->smem_optin) Rb += 2;
+        R = Rb;
         off = layout(R);
     }
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
@@ -761,7 +773,7 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
         return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
     Launch Lc;
     bool ghost_on = params->ghost_enabled && !entries_in && sh->gn > 0;
-    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc, (cudaStream_t)stream);
+    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc, (cudaStream_t)stream, n);
     if (rc) return rc;
     KArgs& A = Lc.A;
     A.stage = stage;
@@ -794,7 +806,7 @@ int pw_search_dataflow(pw_shard* sh, const pw_params* params, const pw_tuning* t
     if (N > 1 && (!inbox || !next_inbox)) return set_err(PW_EINVAL, "dataflow ring needs inboxes");
     Launch Lc;
     const bool ghost_on = params->ghost_enabled && sh->gn > 0;  // stage-0 tasks only
-    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc, (cudaStream_t)stream);
+    int rc = prepare(sh, *params, tuning, false, 0, ghost_on, Lc, (cudaStream_t)stream, q);
     if (rc) return rc;
     KArgs& A = Lc.A;
     A.df = 1;
