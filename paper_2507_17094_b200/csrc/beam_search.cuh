@@ -532,6 +532,29 @@ __device__ __forceinline__ float pw_row4_u8(const uint8_t* x, const float2 (&qr)
     return finish<M>(__fadd_rn(a, __shfl_xor_sync(0xffffffffu, a, 2)));
 }
 
+// uint8 rows against an integer-valued query in [0, 255] (the SIFT case):
+// every (x - q)^2 is an exact integer <= 65025 and every partial sum of <= 258
+// of them stays below 2^24, so numpy's float32 pairwise sum IS the exact
+// integer sum, in any order.  Computed as sum x^2 - 2 sum x q + sum q^2 with
+// DP4A (4 bytes per instruction) and converted once -- bit-identical to
+// pw_row4_u8.  Lane c owns words 4p + c of the row.
+template <int N>
+__device__ __forceinline__ float pw_row4_u8i(const uint8_t* x, const uint32_t (&qw)[N / 16], unsigned c,
+                                             int qsq) {
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(x);
+    unsigned sxx = 0, sxq = 0;
+#pragma unroll
+    for (int p = 0; p < N / 16; p++) {
+        const uint32_t w = xw[4 * p + c];
+        sxx = __dp4a(w, w, sxx);
+        sxq = __dp4a(w, qw[p], sxq);
+    }
+    int t = (int)sxx - 2 * (int)sxq;
+    t += __shfl_xor_sync(0xffffffffu, t, 1);
+    t += __shfl_xor_sync(0xffffffffu, t, 2);
+    return (float)(t + qsq);
+}
+
 template <int M, int OFF, int N>
 __device__ __forceinline__ float pw_sum4(const float* x, const float* q, unsigned c) {
     if constexpr (N <= 128) {
@@ -884,7 +907,7 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
 // completion on a per-half mbarrier, two halves in flight), and 16 rows are
 // reduced per warp pass in the compile-time pairwise order.  D == 0: generic
 // d (cp.async + runtime pairwise plan).
-template <int D, typename VT, int M>
+template <int D, typename VT, int M, bool QI = false>
 __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n, uint64_t thr) {
     const unsigned lane = lane_id();
     int ns = 0;  // survivors (key < thr, search.py:182-184) compacted into ckey as produced
@@ -922,12 +945,20 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             cp_commit();
         };
         const unsigned v = lane >> 2, c = lane & 3u;
-        constexpr bool QREG = (D <= 128 && D % 8 == 0) || sizeof(VT) == 1;
+        constexpr bool QREG = !QI && ((D <= 128 && D % 8 == 0) || sizeof(VT) == 1);
         float2 qr[QREG ? D / 8 : 1];
         if constexpr (QREG) {
             const float2* q2 = reinterpret_cast<const float2*>(S.q);
 #pragma unroll
             for (int p = 0; p < D / 8; p++) qr[p] = q2[4 * p + c];
+        }
+        uint32_t qw[QI ? D / 16 : 1];
+        int qsq = 0;
+        if constexpr (QI) {
+            const uint32_t* qb = reinterpret_cast<const uint32_t*>(S.q + ((D + 3) & ~3));
+#pragma unroll
+            for (int p = 0; p < D / 16; p++) qw[p] = qb[4 * p + c];
+            qsq = reinterpret_cast<const int32_t*>(qb)[((D + 15) & ~15) / 4];
         }
         // one 8-row pass: distance -> key -> survivor compaction
         auto emit = [&](int r0, int rows, float dist) {
@@ -950,7 +981,9 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             for (int pass = 0; pass < rows; pass += 8) {
                 const int rc = pass + (int)v < rows ? pass + (int)v : rows - 1;
                 float dist;
-                if constexpr (sizeof(VT) == 1)
+                if constexpr (QI)
+                    dist = pw_row4_u8i<D>(reinterpret_cast<const uint8_t*>(base + (size_t)rc * sp), qw, c, qsq);
+                else if constexpr (sizeof(VT) == 1)
                     dist = pw_row4_u8<M, D>(reinterpret_cast<const uint8_t*>(base + (size_t)rc * sp), qr, c);
                 else if constexpr (QREG)
                     dist = pw_row4_qreg<M, D>(reinterpret_cast<const float*>(base + (size_t)rc * sp), qr, c);
@@ -1570,7 +1603,15 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
             S.c_dc += n_new;
             PW_T(7);
             const uint64_t thr = S.qlen == C.L ? S.qk0[C.L - 1] : ~0ull;
-            const int ns = score_rows<D, VT, M>(A, S, G, n_new, thr);
+            int ns;
+            if constexpr (sizeof(VT) == 1 && M == 0 && D > 0) {
+                const int32_t* qmeta = reinterpret_cast<const int32_t*>(
+                    reinterpret_cast<const uint8_t*>(S.q + ((D + 3) & ~3)) + ((D + 15) & ~15));
+                ns = qmeta[1] ? score_rows<D, VT, M, true>(A, S, G, n_new, thr)
+                              : score_rows<D, VT, M, false>(A, S, G, n_new, thr);
+            } else {
+                ns = score_rows<D, VT, M>(A, S, G, n_new, thr);
+            }
             PW_T(1);
             inserted = merge_queue(A, S, C, ns);
             PW_T(2);
@@ -1678,6 +1719,31 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
         }
         // query row -> smem
         for (int t = lane; t < A.d; t += 32) S.q[t] = A.queries[(size_t)row * A.d + t];
+        if constexpr (sizeof(VT) == 1 && M == 0 && D > 0) {
+            // the query's bytes, sum q^2 and whether it is integer-valued in
+            // [0, 255] (then pw_row4_u8i is exact; else the float path runs)
+            uint8_t* qb = reinterpret_cast<uint8_t*>(S.q + ((D + 3) & ~3));
+            bool ok = true;
+            int sq = 0;
+            for (int t = lane; t < ((D + 15) & ~15); t += 32) {
+                uint32_t b = 0;
+                if (t < D) {
+                    const float v = A.queries[(size_t)row * A.d + t];
+                    ok &= v >= 0.f && v <= 255.f && v == rintf(v);
+                    b = ok ? (uint32_t)v : 0u;
+                    sq += (int)(b * b);
+                }
+                qb[t] = (uint8_t)b;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            const bool all = __all_sync(0xffffffffu, ok);
+            if (lane == 0) {
+                int32_t* qmeta = reinterpret_cast<int32_t*>(qb + ((D + 15) & ~15));
+                qmeta[0] = sq;
+                qmeta[1] = all ? 1 : 0;
+            }
+        }
         // the task's (qid, stage) wait in shared memory instead of registers
         // across the search: the hot loop runs at the 128-register cap
         int32_t* tsk = S.misc + A.o_par - 2;

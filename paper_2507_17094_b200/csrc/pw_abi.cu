@@ -501,7 +501,10 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         A.PG = PG;
         auto al = [](int64_t x) { return (x + 15) / 16 * 16; };
         int64_t off = 0;
-        A.o_q = (int32_t)off; off = al(off + 4 * (int64_t)((d + 3) & ~3));
+        // query (f32); uint8-row shards also keep the query's bytes and
+        // (sum q^2, integral flag) for the exact integer distance path
+        A.o_q = (int32_t)off;
+        off = al(off + 4 * (int64_t)((d + 3) & ~3) + (elem == 1 ? ((d + 15) & ~15) + 16 : 0));
         A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
         A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
         A.o_newl = (int32_t)off; off = al(off + 4 * cb);

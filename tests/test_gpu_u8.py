@@ -88,3 +88,26 @@ def test_u8_squared_l2_primitive():
         torch.cuda.synchronize()
         want = oracle.squared_l2(x, q)
         assert np.array_equal(out.cpu().numpy(), want), d
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [128, 96])
+@pytest.mark.parametrize("shift", ["fraction", "out_of_range", "mixed"])
+def test_u8_rows_nonintegral_queries_match_oracle(u8sets, d, shift):
+    """Byte rows against queries that are NOT integers in [0, 255]: K1 must take
+    the float path (pw_row4_u8) instead of the exact DP4A integer path, per
+    query; a batch mixing both kinds exercises the per-task switch."""
+    queries, ctxs = u8sets[d]
+    q = queries.copy()
+    if shift == "fraction":
+        q += np.float32(0.25)
+    elif shift == "out_of_range":
+        q[:, 0] = 300.0
+    else:
+        q[::2] += np.float32(0.5)
+    for arm in (0, 1):
+        params = SearchParams(**ARMS[arm])
+        for mode, runner in (("baseline", pw.run_sharded_baseline), ("pipelined", pw.run_pipelined)):
+            got = result_dict(runner(pw.Dataset(q), None, None, params, contexts=ctxs))
+            want = oracle_dict(oracle.run(q, ctxs, params, mode))
+            assert_run_equal(got, want, f"u8 {shift} d={d} arm={arm} {mode}")
