@@ -21,6 +21,8 @@ ap.add_argument("--l", type=int, default=160)
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--tuning", default="", help="JSON object or list of objects")
 ap.add_argument("--arms", default="naive,pathweaver")
+ap.add_argument("--discard", type=float, default=0.5)
+ap.add_argument("--ghost-iter", type=int, default=8)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 tunings = json.loads(args.tuning) if args.tuning else [None]
@@ -36,7 +38,7 @@ for tuning in tunings:
     for arm, mode in (("naive", "baseline"), ("pathweaver", "pipelined")):
         if arm not in args.arms:
             continue
-        p = bench.arm_params(arm, args.l, cfg["k"])
+        p = bench.arm_params(arm, args.l, cfg["k"], discard=args.discard, ghost_iter=args.ghost_iter)
         for _ in range(3):
             dv.run_local([shard], p, q, mode, run, tuning=tuning)
         torch.cuda.synchronize()

@@ -22,6 +22,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--l", type=int, default=256)
 ap.add_argument("--tuning", default="")
+ap.add_argument("--discard", type=float, default=0.5)
+ap.add_argument("--ghost-iter", type=int, default=8)
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 tuning = json.loads(args.tuning) if args.tuning else None
@@ -33,7 +35,7 @@ run = dv.DeviceRun(q.shape[0], 1, cfg["k"], "cuda")
 lib = _abi.load()
 out = (C.c_int64 * 8)()
 for arm, mode in (("pathweaver", "pipelined"), ("naive", "baseline")):
-    p = bench.arm_params(arm, args.l, cfg["k"])
+    p = bench.arm_params(arm, args.l, cfg["k"], discard=args.discard, ghost_iter=args.ghost_iter)
     dv.run_local([shard], p, q, mode, run, tuning=tuning)
     torch.cuda.synchronize()
     _abi.check(lib.pw_phase_cycles(shard.handle, out, 1))
