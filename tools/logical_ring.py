@@ -1,0 +1,113 @@
+"""N-shard PathWeaver vs naive sharding with all N shards on ONE GPU (logical
+shards): the algorithmic side of the multi-GPU target, measured where only
+one GPU is available.
+
+For N in --ns, the C2 dataset (10M x 96) is partitioned into N shards, each
+with its own graph, ghost index, direction table and inter-shard table
+(bench.build_workload with world=N).  Both arms are tuned to recall@10 >= 0.95
+exactly as bench.py does (naive: l; PathWeaver: (discard, ghost_max_iter, l)).
+Times are GPU time on one B200 for the whole batch:
+  naive       every shard searches every query (run_local "baseline"),
+  pathweaver  the ring schedule (run_local "pipelined": chunk c stage s on
+              shard (c+s)%N, entry forwarded) and the dataflow ring
+              (LocalDataflow: N persistent kernels, inbox hand-over).
+On N GPUs each shard's work runs on its own GPU, so with balanced shards the
+N-GPU step time is about this time / N for both arms; the PW/naive ratio is
+the projection (communication: 8 bytes per query per stage, not modelled).
+
+    python tools/logical_ring.py --config c2 --ns 2,4,8
+"""
+import argparse
+import dataclasses
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2507_17094_b200 import builder, device as dv  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--ns", default="2,4,8")
+ap.add_argument("--reps", type=int, default=3)
+args = ap.parse_args()
+cfg = bench.CONFIGS[args.config]
+dev = torch.device("cuda", 0)
+tuning = {"flags": 2}
+k = cfg["k"]
+
+
+def timed(fn):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / args.reps
+
+
+for N in (int(x) for x in args.ns.split(",")):
+    shards, truth, q = [], None, None
+    for r in range(N):
+        W = bench.build_workload(cfg, r, N, dev)
+        if truth is None:
+            truth = bench.ground_truth(W, k)
+            q = W["queries"]
+        gh = W["ghost"] or (None, None)
+        shards.append(dv.TensorShard(W["vec"], W["adj"], W["rows"].to(torch.int32), W["direction"],
+                                     W["inter"], gh[0], gh[1]))
+        del W
+        torch.cuda.empty_cache()
+    run = dv.DeviceRun(q.shape[0], N, k, dev)
+    df = dv.LocalDataflow(shards, q.shape[0], k, dev)
+
+    def recall(p, how):
+        if how == "dataflow":
+            df.run(p, q, run, tuning=tuning)
+        else:
+            dv.run_local(shards, p, q, how, run, tuning=tuning)
+        torch.cuda.synchronize()
+        return builder.recall_at_k(run.final_ids.cpu().numpy(), truth, bench.RECALL_AT)
+
+    out = {"n_shards": N, "queries": q.shape[0]}
+    # naive: smallest l reaching 0.95
+    for l in bench.L_GRID:
+        p = bench.arm_params("naive", l, k)
+        rec = recall(p, "baseline")
+        if rec >= 0.95:
+            break
+    out["naive"] = {"l": l, "recall": round(rec, 4),
+                    "ms": round(timed(lambda: dv.run_local(shards, p, q, "baseline", run, tuning=tuning)), 3)}
+    best = None
+    for how in ("pipelined", "dataflow"):
+        for dr, gi in bench.PW_GRID:
+            for l in bench.L_GRID:
+                pp = bench.arm_params("pathweaver", l, k, discard=dr, ghost_iter=gi)
+                rec = recall(pp, how)
+                if rec >= 0.95:
+                    break
+            if rec < 0.95:
+                continue
+            if how == "dataflow":
+                ms = timed(lambda: df.run(pp, q, run, tuning=tuning))
+            else:
+                ms = timed(lambda: dv.run_local(shards, pp, q, "pipelined", run, tuning=tuning))
+            cand = {"schedule": how, "discard": dr, "ghost_max_iter": gi, "l": l, "recall": round(rec, 4),
+                    "ms": round(ms, 3)}
+            if best is None or ms < best["ms"]:
+                best = cand
+    out["pathweaver"] = best
+    out["pw_over_naive"] = round(out["naive"]["ms"] / best["ms"], 3) if best else None
+    out["projected_qps_n_gpus"] = {
+        "naive": round(q.shape[0] / (out["naive"]["ms"] / N) * 1e3),
+        "pathweaver": round(q.shape[0] / (best["ms"] / N) * 1e3) if best else None}
+    print(json.dumps(out), flush=True)
+    del shards, run, df
+    torch.cuda.empty_cache()
