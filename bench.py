@@ -66,7 +66,7 @@ CONFIGS = {
     "tiny": dict(workload="smoke 20K x 96", n=20_000, d=96, nq=1_000, k=10, j=32, gen="latent",
                  m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=8),
 }
-L_GRID = (32, 48, 64, 96, 128, 160, 192, 256, 320, 384, 512)
+L_GRID = (32, 48, 64, 80, 96, 112, 128, 144, 160, 176, 192, 224, 256, 288, 320, 384, 512)
 # lossy visited cache (K1 tuning flag 2): same ids/distances/counters as the
 # exact set except distance_computations; both arms use it
 DEFAULT_TUNING = '{"flags": 2}'
