@@ -30,7 +30,8 @@ W = bench.build_workload(cfg, 0, 1, torch.device("cuda", 0))
 gh = W["ghost"] or (None, None)
 shard = dv.TensorShard(W["vec"], W["adj"], W["rows"].to(torch.int32), W["direction"], None, gh[0], gh[1])
 run = dv.DeviceRun(W["queries"].shape[0], 1, cfg["k"], "cuda")
-p = bench.arm_params(args.arm, args.l, cfg["k"], discard=args.discard, ghost_iter=args.ghost_iter)
+p = bench.arm_params(args.arm, args.l, cfg["k"], cfg.get("metric", "l2"), discard=args.discard,
+                     ghost_iter=args.ghost_iter)
 mode = "pipelined" if args.arm == "pathweaver" else "baseline"
 import json
 tuning = json.loads(args.tuning) if args.tuning else None
