@@ -25,6 +25,7 @@ from .data import (
     DataFormatError,
     Dataset,
     file_size_for,
+    gen_synthetic,
     load_fvecs,
     load_fvecs_device,
     load_ivecs,

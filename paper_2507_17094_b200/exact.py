@@ -212,7 +212,7 @@ def build_index(dataset, n_shards: int, j: int, seed: int, *, rho: float = 0.01,
     ids = np.arange(data.shape[0], dtype=np.int32) if ids is None else np.asarray(ids, np.int32)
     rows = partition_rows(data.shape[0], n_shards, seed)
     j_g = min(j, 16) if ghost_degree is None else ghost_degree
-    xs = torch.from_numpy(data).to(dev)
+    xs = torch.from_numpy(data if data.flags.writeable else data.copy()).to(dev)
     report = BuildReport()
     packs = []
 
