@@ -268,7 +268,7 @@ def exact_knn_batch(base, queries, k: int, ids=None) -> tuple[np.ndarray, np.nda
         raise ValueError(f"query dimension {q.shape} does not match dataset d={data.shape[1]}")
     if not 1 <= k <= data.shape[0]:
         raise ValueError(f"k must be in [1, {data.shape[0]}], got {k}")
-    xb = torch.from_numpy(data).cuda()
+    xb = torch.from_numpy(data if data.flags.writeable else data.copy()).cuda()
     xq = torch.from_numpy(q).cuda()
     loc, sq = exact_topk(xb, xq, k)
     loc = loc.cpu().numpy()
