@@ -269,7 +269,7 @@ def exact_knn_batch(base, queries, k: int, ids=None) -> tuple[np.ndarray, np.nda
     if not 1 <= k <= data.shape[0]:
         raise ValueError(f"k must be in [1, {data.shape[0]}], got {k}")
     xb = torch.from_numpy(data if data.flags.writeable else data.copy()).cuda()
-    xq = torch.from_numpy(q).cuda()
+    xq = torch.from_numpy(q if q.flags.writeable else q.copy()).cuda()
     loc, sq = exact_topk(xb, xq, k)
     loc = loc.cpu().numpy()
     out_ids = loc.astype(np.int32) if gids is None else np.asarray(gids, np.int32)[loc]

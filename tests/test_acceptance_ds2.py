@@ -156,3 +156,92 @@ def test_ds4_ghost_staging_iterations():
 
     assert iters_to_090(False, range(8, 45)) == (22, 17.11)
     assert iters_to_090(True, range(3, 30)) == (8, 11.77)
+
+
+@pytest.mark.gpu
+def test_inter_shard_and_direction_exactness():
+    """Criterion 10: the GPU-built inter-shard table is the brute-force argmin
+    into the next shard (8000/8000) and every direction word is the packed
+    sign rule (64000/64000 edges); brute force in numpy here."""
+    from paper_2507_17094_b200 import exact
+
+    full = pw.gen_synthetic(8000, 16, 512, 0.1, seed=33)
+    index, _ = exact.build_index(full, 4, 8, seed=13, with_ghost=False)
+    ctxs = pw.build_contexts(index, full)
+    inter_ok = dir_ok = 0
+    for s in range(4):
+        x, y = ctxs[s].vectors.astype(np.float64), ctxs[(s + 1) % 4].vectors.astype(np.float64)
+        d2 = (x * x).sum(1)[:, None] - 2 * x @ y.T + (y * y).sum(1)[None, :]
+        inter_ok += int((ctxs[s].inter_map == d2.argmin(1)).sum())
+        want = gu.direction_table(ctxs[s].vectors, ctxs[s].adj)
+        dir_ok += int((index.shards[s].direction == want).all(axis=2).sum())
+    assert (inter_ok, dir_ok) == (8000, 64000)
+
+
+@pytest.mark.gpu
+def test_format_fidelity(tmp_path):
+    """Criterion 11: fvecs/ivecs round trips byte-identical, index round trip
+    value-identical with checksum verification (host and device loaders),
+    corruption detected."""
+    from paper_2507_17094_b200 import exact
+    from paper_2507_17094_b200.container import ChecksumError
+
+    rng = np.random.default_rng(9)
+    vecs = rng.standard_normal((500, 24)).astype(np.float32)
+    ids = rng.integers(0, 10_000, (500, 10)).astype(np.int32)
+    f1, f2, i1, i2 = (tmp_path / n for n in ("a.fvecs", "b.fvecs", "a.ivecs", "b.ivecs"))
+    pw.save_fvecs(vecs, f1)
+    pw.save_fvecs(pw.load_fvecs(f1), f2)
+    pw.save_ivecs(ids, i1)
+    pw.save_ivecs(pw.load_ivecs(i1), i2)
+    assert f1.read_bytes() == f2.read_bytes() and i1.read_bytes() == i2.read_bytes()
+
+    full = pw.gen_synthetic(2000, 16, 64, 0.1, seed=44)
+    index, _ = exact.build_index(full, 2, 8, seed=3, rho=0.05, ghost_degree=4)
+    path = tmp_path / "rt.pwix"
+    pw.serialize_index(index, path)
+    assert pw.index_equal(index, pw.deserialize_index(path))
+    dev = pw.load_index_device(path)
+    for sh, pack in zip(dev.shards, index.shards):
+        assert np.array_equal(sh["adj"].cpu().numpy(), pack.adj)
+    blob = bytearray(path.read_bytes())
+    blob[-3] ^= 0x40
+    path.write_bytes(bytes(blob))
+    with pytest.raises(ChecksumError):
+        pw.deserialize_index(path)
+    with pytest.raises(ChecksumError):
+        pw.load_index_device(path)
+
+
+@pytest.mark.gpu
+def test_complete_graph_exact():
+    """Criterion 01: on a complete graph (256 points, j = 255) the search
+    returns the exact top 10 for all 32 queries."""
+    import torch
+
+    from paper_2507_17094_b200 import exact, metrics
+    from paper_2507_17094_b200.graphs import Index, ShardPack
+
+    full = pw.gen_synthetic(288, 16, 32, 0.25, seed=5)
+    base = pw.Dataset(full.data[:256])
+    queries = pw.Dataset(full.data[256:])
+    adj = exact.build_knn_graph(torch.from_numpy(np.array(base.data)).cuda(), 255).cpu().numpy()
+    index = Index(d=16, n_total=256, shards=[ShardPack(base.ids, adj, None, None, None, None)])
+    res = pw.run_sharded_baseline(queries, index, base, pw.SearchParams(k=10, l=64, m=64, r=8, max_iter=16, seed=3))
+    truth = metrics.exact_knn_batch(base, queries, 10)
+    assert all(metrics.recall_at_k(t, r, 10) == 1.0 for t, r in zip(truth, res.neighbor_lists()))
+
+
+@pytest.mark.gpu
+def test_determinism_across_threads_and_reruns(ds2):
+    """Criterion 09: results and metric totals identical across threads=1 /
+    threads=8 / a rerun with the same seed."""
+    from paper_2507_17094_b200 import metrics
+
+    p = ds2["params"]
+    runs = [pw.run_pipelined(ds2["queries"], ds2["index"], ds2["base"], p, threads=t, contexts=ds2["ctxs"])
+            for t in (1, 8, 1)]
+    for r in runs[1:]:
+        assert np.array_equal(r.final_ids, runs[0].final_ids)
+        assert np.array_equal(r.final_dists, runs[0].final_dists)
+        assert metrics.collect_metrics(r).totals_dict() == metrics.collect_metrics(runs[0]).totals_dict()
