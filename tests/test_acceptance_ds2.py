@@ -245,3 +245,54 @@ def test_determinism_across_threads_and_reruns(ds2):
         assert np.array_equal(r.final_ids, runs[0].final_ids)
         assert np.array_equal(r.final_dists, runs[0].final_dists)
         assert metrics.collect_metrics(r).totals_dict() == metrics.collect_metrics(runs[0]).totals_dict()
+
+
+# SURVEY.md V8 (the reference run on BASELINE configs[0], C1): recall@10 >=
+# 0.95 needs l=192 naive (0.9545), l=96 pipelined (0.9503), l=128 pipelined +
+# ghost + DGS (0.9590) at 2 shards; distance computations per query at that
+# point, naive vs pipelined + ghost + DGS, for 2 / 4 / 8 shards.
+C1_GRID = (32, 48, 64, 96, 128, 192, 256, 384)
+C1_V8_DC = {2: (4855, 2786), 4: (8784, 2453), 8: (11827, 3585)}
+
+
+@pytest.fixture(scope="module")
+def c1():
+    from paper_2507_17094_b200 import metrics
+
+    full = pw.gen_synthetic(101_000, 128, 8192, 0.08, seed=0)
+    base = pw.Dataset(full.data[:100_000])
+    queries = pw.Dataset(full.data[100_000:])
+    return dict(base=base, queries=queries, truth=metrics.exact_knn_batch(base, queries, 10))
+
+
+def _c1_point(c1, index, ctxs, params, mode):
+    from paper_2507_17094_b200 import metrics
+
+    runner = pw.run_pipelined if mode == "pipelined" else pw.run_sharded_baseline
+    for l in C1_GRID:
+        res = runner(c1["queries"], index, c1["base"], params.with_(l=l), contexts=ctxs)
+        rec = metrics.mean_recall(c1["truth"], res.neighbor_lists(), 10)
+        if rec >= 0.95:
+            return l, rec, metrics.collect_metrics(res).distance_computations / c1["queries"].n
+    return None
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_shards", [2, 4, 8])
+def test_c1_operating_points_match_reference(c1, n_shards):
+    from paper_2507_17094_b200 import exact
+
+    index, _ = exact.build_index(c1["base"], n_shards, 32, seed=0, rho=0.01, ghost_degree=16)
+    ctxs = pw.build_contexts(index, c1["base"])
+    p = pw.SearchParams(k=10, l=64, m=64, r=8, max_iter=64, seed=0)
+    pw_p = p.with_(ghost_enabled=True, ghost_max_iter=8, selection="direction", discard_ratio=0.5,
+                   cooldown_ratio=0.3)
+    naive = _c1_point(c1, index, ctxs, p, "baseline")
+    pwv = _c1_point(c1, index, ctxs, pw_p, "pipelined")
+    if n_shards == 2:
+        pipe = _c1_point(c1, index, ctxs, p, "pipelined")
+        assert (naive[0], round(naive[1], 4)) == (192, 0.9545)
+        assert (pipe[0], round(pipe[1], 4)) == (96, 0.9503)
+        assert (pwv[0], round(pwv[1], 4)) == (128, 0.959)
+    want_naive, want_pw = C1_V8_DC[n_shards]
+    assert (round(naive[2]), round(pwv[2])) == (want_naive, want_pw), (naive, pwv)
