@@ -95,9 +95,13 @@ def crc32c_device(buffers, stream=None) -> list[int]:
             raise ValueError("crc32c_device needs contiguous CUDA tensors")
         ptrs[i] = b.data_ptr() if b.numel() else None
         lens[i] = b.numel() * b.element_size()
+    devs = {b.device for b in buffers}
+    if len(devs) != 1:
+        raise ValueError("crc32c_device: all buffers must be on one device")
     out = (C.c_uint32 * n)()
-    st = stream if stream is not None else torch.cuda.current_stream()
-    _abi.check(lib.pw_crc32c_device(ptrs, lens, n, out, C.c_void_p(st.cuda_stream)))
+    with torch.cuda.device(devs.pop()):
+        st = stream if stream is not None else torch.cuda.current_stream()
+        _abi.check(lib.pw_crc32c_device(ptrs, lens, n, out, C.c_void_p(st.cuda_stream)))
     return [int(x) for x in out]
 
 
