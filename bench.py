@@ -43,7 +43,7 @@ CONFIGS = {
     # gen_synthetic family (uniform centres + spread * N(0, I)).
     "c2": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph",
                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
-               spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192),
+               spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
     "c1": dict(workload="SIFT-shaped 100K x 128 f32, 1K queries, k=10, degree-32 graph",
                n=100_000, d=128, nq=1_000, k=10, j=32, gen="gauss", n_clusters=8192,
                spread=0.08, rho=0.01, j_g=16, probe=32, builder="exact"),
@@ -55,22 +55,23 @@ CONFIGS = {
     "c3s": dict(workload="SIFT-shaped 12.5M x 128 uint8 (one of C3's 8 shards of 100M), 10K queries, "
                          "k=10, degree-32 graph", n=12_500_000, d=128, nq=10_000, k=10, j=32,
                 gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192,
-                dtype="u8"),
+                refine=1, dtype="u8"),
     "c4": dict(workload="GIST-shaped 1M x 960 f32, 1K queries, k=10, degree-32 graph", n=1_000_000,
                d=960, nq=1_000, k=10, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05,
                rho=0.01, j_g=16, probe=48, builder="exact"),
     "c5s": dict(workload="Text2Image-shaped 12.5M x 200 f32 inner product (one of C5's 8 shards of "
                          "100M), 10K queries, k=100, degree-32 graph", n=12_500_000, d=200, nq=10_000,
                 k=100, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01,
-                j_g=16, probe=192, metric="ip"),
+                j_g=16, probe=192, refine=1, metric="ip"),
     "tiny": dict(workload="smoke 20K x 96", n=20_000, d=96, nq=1_000, k=10, j=32, gen="latent",
                  m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=8),
 }
-# IVF probe of the approximate 10M+ graph builder: the reference's graph is
-# the exact kNN graph (graphs.py:104-134); probe 192 keeps 69% of the exact
-# 32-NN rows' entries at C2 (48: 42%) for ~30 s more setup, and lowers both
-# arms' operating points (tools/graph_probe.py: naive l 256 -> 144, PW l 256
-# -> 160; K1 4.84 -> 3.39 / 2.77 -> 1.98 ms).
+# IVF probe + neighbour-of-neighbour refinement of the approximate 10M+ graph
+# builder: the reference's graph is the exact kNN graph (graphs.py:104-134).
+# At C2 (tools/graph_probe.py) each row keeps this share of its exact 32-NN:
+# probe 48 42%, 192 69%, 192 + one refinement pass 85% (setup 29 -> 72 s);
+# both arms' operating points fall with it (naive l 256 -> 144 -> 128, PW l
+# 256 -> 160 -> 144; K1 naive 4.84 -> 3.39 -> 3.06, PW 2.77 -> 1.98 -> 1.85 ms).
 L_GRID = (32, 48, 64, 80, 96, 112, 128, 144, 160, 176, 192, 224, 256, 288, 320, 384, 512)
 # lossy visited cache (K1 tuning flag 2): same ids/distances/counters as the
 # exact set except distance_computations; both arms use it
@@ -206,7 +207,8 @@ def build_workload(cfg: dict, rank: int, world: int, device):
         parts = builder.partition(cfg["n"], world, SEED, device=device)
         rows = parts[rank]
         vec = base[rows].contiguous()
-        adj = builder.knn_graph(vec, cfg["j"], probe=cfg["probe"], seed=SEED + rank)
+        adj = builder.knn_graph(vec, cfg["j"], probe=cfg["probe"], seed=SEED + rank,
+                                refine=cfg.get("refine", 0))
         gh = builder.ghost(vec, cfg["rho"], cfg["j_g"], SEED + rank)
         inter = None
         if world > 1:
@@ -478,8 +480,9 @@ def run_ours(args, cfg):
                        "graph": ("exact kNN + reverse augmentation, exact inter-shard and ghost "
                                  "graphs (exact.py, graphs.py semantics); rho=%.2f j_g=%d; direction "
                                  "table" % (cfg["rho"], cfg["j_g"])) if cfg.get("builder") == "exact" else
-                                ("GPU IVF kNN (probe %d) + reverse-edge augmentation; ghost "
-                                 "rho=%.2f j_g=%d; direction table" % (cfg["probe"], cfg["rho"], cfg["j_g"])),
+                                ("GPU IVF kNN (probe %d, refine %d) + reverse-edge augmentation; ghost "
+                                 "rho=%.2f j_g=%d; direction table" % (cfg["probe"], cfg.get("refine", 0),
+                                                                          cfg["rho"], cfg["j_g"])),
                        "sweep": ops["pathweaver"]["sweep"]},
             "e2e": {"value": round(nq * e2e_steps / e2e_s, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
@@ -522,7 +525,8 @@ def traffic_for(cfg: dict, l: int, discard: float = 0.5, ghost_iter: int = 8):
             if t.get("workload") == cfg["workload"] and t.get("l") == l and \
                     float(t.get("dgs_discard", 0.5)) == float(discard) and \
                     int(t.get("ghost_max_iter", 8)) == int(ghost_iter) and \
-                    (cfg.get("builder") == "exact" or int(t.get("probe", 48)) == int(probe)):
+                    (cfg.get("builder") == "exact" or (int(t.get("probe", 48)) == int(probe) and
+                                                       int(t.get("refine", 0)) == int(cfg.get("refine", 0)))):
                 return int(t["traffic_bytes_per_launch"])
     return None
 

@@ -262,7 +262,7 @@ def reverse_augment(x: torch.Tensor, adj: torch.Tensor, chunk: int = 1 << 17) ->
 
 
 def knn_graph(x: torch.Tensor, j: int, probe: int = 8, n_lists: int | None = None,
-              seed: int = 0, augment: bool = True) -> torch.Tensor:
+              seed: int = 0, augment: bool = True, refine: int = 0) -> torch.Tensor:
     n = x.shape[0]
     if n <= 1 << 16:
         adj = exact_knn(x, x, j, exclude_self=True).to(torch.int32)
@@ -274,7 +274,34 @@ def knn_graph(x: torch.Tensor, j: int, probe: int = 8, n_lists: int | None = Non
         bad = adj < 0
         if bad.any():  # rows with too few candidates: fall back to repeating row[0]
             adj = torch.where(bad, adj[:, :1].expand_as(adj), adj)
+        if refine:
+            adj = refine_knn(x, adj, refine)
     return reverse_augment(x, adj) if augment else adj
+
+
+def refine_knn(x: torch.Tensor, adj: torch.Tensor, iters: int = 1, chunk: int = 8192) -> torch.Tensor:
+    """Neighbour-of-neighbour refinement of an approximate j-NN graph (one
+    NN-descent style pass per iteration): each row keeps the j nearest of
+    its neighbours and their neighbours.  Moves the IVF graph toward the
+    reference's exact kNN graph (graphs.py:104-134)."""
+    n, j = adj.shape
+    dev = x.device
+    for _ in range(iters):
+        new = torch.empty_like(adj)
+        for lo in range(0, n, chunk):
+            hi = min(n, lo + chunk)
+            a = adj[lo:hi].long()
+            cand = torch.cat([a, adj[a.reshape(-1)].long().reshape(hi - lo, j * j)], 1)
+            cs = torch.sort(cand, 1).values
+            drop = torch.zeros_like(cs, dtype=torch.bool)
+            drop[:, 1:] = cs[:, 1:] == cs[:, :-1]
+            drop |= cs == torch.arange(lo, hi, device=dev)[:, None]
+            d2 = ((x[cs] - x[lo:hi, None, :]) ** 2).sum(-1)
+            d2.masked_fill_(drop, float("inf"))
+            top = torch.topk(d2, j, dim=1, largest=False).indices
+            new[lo:hi] = torch.gather(cs, 1, top).to(adj.dtype)
+        adj = new
+    return adj
 
 
 def exact_knn(base: torch.Tensor, queries: torch.Tensor, k: int, exclude_self: bool = False,

@@ -20,10 +20,11 @@ from paper_2507_17094_b200 import builder, device as dv  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--probes", default="48,96,192")
+ap.add_argument("--refines", default="0")
 args = ap.parse_args()
 tuning = {"flags": 2}
-for probe in (int(x) for x in args.probes.split(",")):
-    cfg = dict(bench.CONFIGS[args.config], probe=probe)
+for probe, refine in ((int(p), int(r)) for p in args.probes.split(",") for r in args.refines.split(",")):
+    cfg = dict(bench.CONFIGS[args.config], probe=probe, refine=refine)
     t0 = time.time()
     W = bench.build_workload(cfg, 0, 1, torch.device("cuda", 0))
     build_s = time.time() - t0
@@ -38,7 +39,7 @@ for probe in (int(x) for x in args.probes.split(",")):
     shard = dv.TensorShard(W["vec"], W["adj"], W["rows"].to(torch.int32), W["direction"], None, gh[0], gh[1])
     q = W["queries"]
     run = dv.DeviceRun(q.shape[0], 1, cfg["k"], "cuda")
-    out = {"probe": probe, "build_s": round(build_s, 1), "graph_recall_at_j": round(acc, 4)}
+    out = {"probe": probe, "refine": refine, "build_s": round(build_s, 1), "graph_recall_at_j": round(acc, 4)}
     for arm, mode, kw in (("naive", "baseline", {}), ("pathweaver", "pipelined", dict(discard=0.8, ghost_iter=1))):
         for l in bench.L_GRID:
             p = bench.arm_params(arm, l, cfg["k"], **kw)
