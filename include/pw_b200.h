@@ -197,6 +197,12 @@ int pw_search_dataflow(pw_shard* shard, const pw_params* params, const pw_tuning
 int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, const int64_t* ib,
                 int64_t n, float* out, void* stream);
 
+/* Validate a shard's inter_map (pipeline.py:339 forwards inter_map[top1]
+ * as the next shard's entry) against the next shard's size n_next: every
+ * value must be in [0, n_next).  Synchronous once per (shard, n_next);
+ * pw_run / pw_run_device call it for every pipelined ring.  0 or PW_EINVAL. */
+int pw_shard_validate_inter(pw_shard* shard, int64_t n_next);
+
 /* Synchronous check of a shard's device error flag (table overflow, a
  * dataflow inbox that never filled); clears it.  0 or PW_ECUDA + message. */
 int pw_shard_check(pw_shard* shard);

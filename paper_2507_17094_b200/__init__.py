@@ -21,17 +21,7 @@ from .container import (
     load_index_device,
     serialize_index,
 )
-from .data import (
-    DataFormatError,
-    Dataset,
-    file_size_for,
-    gen_synthetic,
-    load_fvecs,
-    load_fvecs_device,
-    load_ivecs,
-    save_fvecs,
-    save_ivecs,
-)
+from .data import DataFormatError, Dataset
 from .graphs import Index, ShardPack, words_per_vector
 from .pipeline import (
     NeighborList,

@@ -87,6 +87,7 @@ EXPORTS = {
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.c_int32, C.c_void_p]),
     "pw_shard_check": (C.c_int, [C.c_void_p]),
+    "pw_shard_validate_inter": (C.c_int, [C.c_void_p, C.c_int64]),
     "pw_l2_pairs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
                               C.c_void_p, C.c_void_p]),
     "pw_dev_alloc": (C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),

@@ -108,11 +108,15 @@ def crc32c_device(buffers, stream=None) -> list[int]:
 # ---------------------------------------------------------------- serialize --
 
 def _has_padded_rows(adj) -> bool:
-    """container.py:60-65: True when any adjacency row repeats a neighbor."""
-    if adj is None or adj.shape[1] < 2:
+    """The container's "padded" meta flag (container.py:60-65): some row
+    lists a neighbour twice (degree-deficit padding repeats ids).  A row
+    repeats an id iff it has fewer distinct values than slots."""
+    if adj is None or adj.size == 0:
         return False
-    rows = np.sort(adj, axis=1)
-    return bool((rows[:, 1:] == rows[:, :-1]).any())
+    a = np.asarray(adj)
+    srt = np.sort(a, axis=1)
+    distinct = 1 + np.count_nonzero(np.diff(srt, axis=1), axis=1)
+    return bool((distinct < a.shape[1]).any())
 
 
 def _host(a):

@@ -197,6 +197,7 @@ struct pw_shard {
     int32_t* gadj = nullptr;
     int32_t* gids = nullptr;
     int64_t bytes = 0;
+    int64_t inter_ok_n = -1;  // inter_map validated against a next shard of this size
     // launch workspace (grow-only)
     int32_t* counter = nullptr;
     unsigned long long* phase = nullptr;  // 8 cycle counters (timer builds)
@@ -234,6 +235,45 @@ __global__ void gather_rows_kernel(const uint8_t* __restrict__ vec, const int32_
     }
 }
 
+// Index validation: count entries of p[0..n) outside [0, hi) and record the
+// first such position (ids become gather indices inside K1, so a bad id in a
+// CRC-valid but inconsistent container must be rejected before any search).
+__global__ void range_check_kernel(const int32_t* __restrict__ p, int64_t n, int64_t hi,
+                                   unsigned long long* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = p[i];
+        if (v < 0 || (int64_t)v >= hi) {
+            atomicAdd(&out[0], 1ull);
+            atomicMin(&out[1], (unsigned long long)i);
+        }
+    }
+}
+
+// Returns PW_EINVAL with "<what> id <v> at <pos> outside [0, hi)" when some
+// entry is out of range (synchronous; shard creation / first pipelined use).
+int check_ids(const int32_t* p, int64_t n, int64_t hi, const char* what) {
+    if (!p || n <= 0) return 0;
+    unsigned long long* d = nullptr;
+    PW_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+    unsigned long long h[2] = {0ull, ~0ull};
+    cudaError_t e = cudaMemcpy(d, h, sizeof h, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        range_check_kernel<<<(int)std::min<int64_t>(4096, (n + 255) / 256), 256>>>(p, n, hi, d);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    int32_t v = 0;
+    if (e == cudaSuccess && h[0]) e = cudaMemcpy(&v, p + h[1], sizeof v, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    g_launches++;
+    if (e != cudaSuccess) return set_err(PW_ECUDA, std::string("index validation: ") + cudaGetErrorString(e));
+    if (h[0])
+        return set_err(PW_EINVAL, std::string(what) + " id " + std::to_string(v) + " at position " +
+                                      std::to_string(h[1]) + " outside shard of " + std::to_string(hi) +
+                                      " nodes (" + std::to_string(h[0]) + " such entries)");
+    return 0;
+}
+
 // K2: per-query best k of n_cols*k candidates by (distance, id)
 // (pipeline.py:187-196).  One warp per query; rank selection in shared memory.
 __global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float* __restrict__ dists,
@@ -267,7 +307,9 @@ __global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float*
         for (int t = lane; t < cnt; t += 32) {
             uint64_t key = keys[t];
             int rank = 0;
-            for (int o = 0; o < cnt; o++) rank += keys[o] < key;
+            // ties on (distance, id) keep candidate order, like the stable
+            // np.lexsort (pipeline.py:195): equal keys get distinct ranks
+            for (int o = 0; o < cnt; o++) rank += keys[o] < key || (keys[o] == key && o < t);
             if (rank < k) {
                 out_ids[qi * k + rank] = (int32_t)(uint32_t)key;
                 out_dists[qi * k + rank] = bits_dist<1>((uint32_t)(key >> 32));
@@ -727,6 +769,7 @@ int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
         return fail(rc);
     if ((rc = upload(&sh->adj, D->adj, (size_t)D->n * D->j, &sh->bytes, od))) return fail(rc);
     if ((rc = upload(&sh->gid, D->global_ids, (size_t)D->n, &sh->bytes, od))) return fail(rc);
+    if ((rc = check_ids(sh->adj, (int64_t)D->n * D->j, D->n, "adjacency"))) return fail(rc);
     if (D->direction &&
         (rc = upload(&sh->dir, D->direction, (size_t)D->n * D->j * sh->W, &sh->bytes, od)))
         return fail(rc);
@@ -740,6 +783,8 @@ int pw_shard_create(const pw_shard_desc* D, pw_shard** out) {
             return fail(rc);
         if ((rc = upload((uint8_t**)&sh->gvec, nullptr, (size_t)D->ghost_n * D->d * elem, &sh->bytes)))
             return fail(rc);
+        if ((rc = check_ids(sh->gids, sh->gn, sh->n, "ghost parent"))) return fail(rc);
+        if ((rc = check_ids(sh->gadj, sh->gn * sh->gj, sh->gn, "ghost adjacency"))) return fail(rc);
         gather_rows_kernel<<<256, 256>>>((const uint8_t*)sh->vec, sh->gids, sh->gn, (int64_t)sh->d * elem,
                                          (uint8_t*)sh->gvec);
         g_launches++;
@@ -846,6 +891,17 @@ int pw_search_dataflow(pw_shard* sh, const pw_params* params, const pw_tuning* t
     return launch(sh, Lc, (cudaStream_t)stream);
 }
 
+int pw_shard_validate_inter(pw_shard* sh, int64_t n_next) {
+    if (!sh) return set_err(PW_EINVAL, "null argument");
+    if (!sh->inter) return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
+    if (sh->inter_ok_n == n_next) return 0;
+    PW_CUDA(cudaSetDevice(sh->device));
+    int rc = check_ids(sh->inter, sh->n, n_next, "inter-shard map");
+    if (rc) return rc;
+    sh->inter_ok_n = n_next;
+    return 0;
+}
+
 int pw_shard_check(pw_shard* sh) {
     if (!sh) return set_err(PW_EINVAL, "null argument");
     if (!sh->counter) return 0;
@@ -949,9 +1005,8 @@ int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
         }
     } else {
         if (N > 1)
-            for (int s = 0; s < N; s++)
-                if (!shards[s]->inter)
-                    return set_err(PW_EINVAL, "pipelined mode requires inter-shard tables for every shard");
+            for (int s = 0; s < N; s++)  // forwarded entries index shard s+1 (pipeline.py:339)
+                if ((rc = pw_shard_validate_inter(shards[s], shards[(s + 1) % N]->n))) return rc;
         std::vector<int64_t> lo(N + 1, 0);  // np.array_split(arange(Q), N)
         for (int c = 0; c < N; c++) lo[c + 1] = lo[c] + q / N + (c < q % N ? 1 : 0);
         int32_t* ein = entries_a;
@@ -981,6 +1036,20 @@ struct RunWs {
     size_t cap = 0;
 };
 RunWs g_ws[64];
+
+// grow-only device buffer of a RunWs (caller holds W.mu)
+int ws_reserve(RunWs& W, size_t bytes) {
+    if (W.cap >= bytes) return 0;
+    if (W.buf) {
+        if (W.st) PW_CUDA(cudaStreamSynchronize(W.st));
+        cudaFree(W.buf);
+    }
+    W.buf = nullptr;
+    W.cap = 0;
+    PW_CUDA(cudaMalloc(&W.buf, bytes));
+    W.cap = bytes;
+    return 0;
+}
 
 int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw_tuning* tuning,
            const float* queries, int64_t q, int32_t mode, int32_t* shard_ids, float* shard_dists,
@@ -1012,13 +1081,7 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
            o_fd = take(sizeof(float) * qq * k), o_s32 = take(sizeof(int32_t) * qq * N * 4),
            o_s64 = take(sizeof(int64_t) * qq * N * 6), o_ea = take(sizeof(int32_t) * qq),
            o_eb = take(sizeof(int32_t) * qq), o_err = take(sizeof(int32_t));
-    if (W.cap < off) {
-        if (W.buf) cudaFree(W.buf);
-        W.buf = nullptr;
-        W.cap = 0;
-        PW_CUDA(cudaMalloc(&W.buf, off));
-        W.cap = off;
-    }
+    if ((rc = ws_reserve(W, off))) return rc;
     char* b = W.buf;
     float* dq = (float*)(b + o_q);
     int32_t* sid = (int32_t*)(b + o_sid);
@@ -1067,8 +1130,17 @@ int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, cons
         if (seeds[i] < 0 || seeds[i] >= n)
             return set_err(PW_EINVAL, "seed " + std::to_string(seeds[i]) + " outside shard of " +
                                           std::to_string(n) + " nodes");
+    PW_CUDA(cudaSetDevice(sh->device));
+    // The shard's launch workspace (task counter, visited tables, scratch) is
+    // shared by every launch on it: searches of one device are serialised on
+    // its run stream, under the same lock as pw_run (the reference's search
+    // is reentrant and run from thread pools, pipeline.py:352-385).
+    RunWs& W = g_ws[sh->device];
+    std::lock_guard<std::mutex> lk(W.mu);
+    if (!W.st) PW_CUDA(cudaStreamCreateWithFlags(&W.st, cudaStreamNonBlocking));
+    cudaStream_t st = W.st;
     Launch Lc;
-    int rc = prepare(sh, *params, nullptr, use_ghost != 0, n_seeds, false, Lc);
+    int rc = prepare(sh, *params, nullptr, use_ghost != 0, n_seeds, false, Lc, st);
     if (rc) return rc;
     KArgs& A = Lc.A;
     const int64_t k = params->k;
@@ -1083,13 +1155,13 @@ int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, cons
            o_r = bump(sizeof(Pcg64)), o_id = bump(sizeof(int32_t) * k), o_d = bump(sizeof(float) * k),
            o_l = bump(sizeof(int32_t) * k), o_rec = bump(sizeof(TaskRecord)),
            o_v = bump(sizeof(int32_t) * std::max<int64_t>(visit_cap, 1));
-    char* buf = nullptr;
-    PW_CUDA(cudaSetDevice(sh->device));
-    PW_CUDA(cudaMalloc(&buf, bytes));
+    if ((rc = ws_reserve(W, bytes))) return rc;
+    char* buf = W.buf;
     Pcg64 g{rng->state_hi, rng->state_lo, rng->inc_hi, rng->inc_lo, (uint32_t)rng->has_uint32, rng->uinteger};
-    cudaMemcpy(buf + o_q, query, sizeof(float) * sh->d, cudaMemcpyHostToDevice);
-    if (n_seeds) cudaMemcpy(buf + o_s, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyHostToDevice);
-    cudaMemcpy(buf + o_r, &g, sizeof g, cudaMemcpyHostToDevice);
+    PW_CUDA(cudaMemcpyAsync(buf + o_q, query, sizeof(float) * sh->d, cudaMemcpyHostToDevice, st));
+    if (n_seeds)
+        PW_CUDA(cudaMemcpyAsync(buf + o_s, seeds, sizeof(int64_t) * n_seeds, cudaMemcpyHostToDevice, st));
+    PW_CUDA(cudaMemcpyAsync(buf + o_r, &g, sizeof g, cudaMemcpyHostToDevice, st));
     A.stage = 0;
     A.q0 = 0;
     A.n_tasks = 1;
@@ -1104,39 +1176,38 @@ int pw_search_one(pw_shard* sh, int32_t use_ghost, const pw_params* params, cons
     A.rec = (TaskRecord*)(buf + o_rec);
     A.visit_log = visit_cap ? (int32_t*)(buf + o_v) : nullptr;
     A.visit_cap = visit_cap;
-    rc = launch(sh, Lc, 0);
-    cudaError_t e = cudaDeviceSynchronize();
-    if (!rc && e != cudaSuccess) rc = set_err(PW_ECUDA, cudaGetErrorString(e));
-    if (!rc) rc = check_err(sh);
-    if (!rc) {
-        TaskRecord R;
-        cudaMemcpy(&R, buf + o_rec, sizeof R, cudaMemcpyDeviceToHost);
-        cudaMemcpy(&g, buf + o_r, sizeof g, cudaMemcpyDeviceToHost);
-        cudaMemcpy(out_ids, buf + o_id, sizeof(int32_t) * R.n_out, cudaMemcpyDeviceToHost);
-        cudaMemcpy(out_dists, buf + o_d, sizeof(float) * R.n_out, cudaMemcpyDeviceToHost);
-        if (out_local) cudaMemcpy(out_local, buf + o_l, sizeof(int32_t) * R.n_out, cudaMemcpyDeviceToHost);
-        if (visit_cap && visit_log)
-            cudaMemcpy(visit_log, buf + o_v, sizeof(int32_t) * std::min<int64_t>(R.n_visited, visit_cap),
-                       cudaMemcpyDeviceToHost);
-        out->iterations = R.c[0];
-        out->distance_computations = R.c[1];
-        out->total_visits = R.c[2];
-        out->nodes_expanded = R.c[3];
-        out->dgs_skipped = R.c[4];
-        out->inserted_total = R.c[5];
-        out->converged = R.converged;
-        out->retained = R.retained;
-        out->n_out = R.n_out;
-        out->n_visited = R.n_visited;
-        rng->state_hi = g.s_hi;
-        rng->state_lo = g.s_lo;
-        rng->inc_hi = g.i_hi;
-        rng->inc_lo = g.i_lo;
-        rng->has_uint32 = (int32_t)g.has32;
-        rng->uinteger = g.u32;
-    }
-    cudaFree(buf);
-    return rc;
+    if ((rc = launch(sh, Lc, st))) return rc;
+    TaskRecord R;
+    PW_CUDA(cudaMemcpyAsync(&R, buf + o_rec, sizeof R, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(&g, buf + o_r, sizeof g, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaStreamSynchronize(st));
+    if ((rc = check_err(sh))) return rc;
+    if (R.n_out < 0 || R.n_out > k) return set_err(PW_ECUDA, "search produced no result record");
+    PW_CUDA(cudaMemcpyAsync(out_ids, buf + o_id, sizeof(int32_t) * R.n_out, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(out_dists, buf + o_d, sizeof(float) * R.n_out, cudaMemcpyDeviceToHost, st));
+    if (out_local)
+        PW_CUDA(cudaMemcpyAsync(out_local, buf + o_l, sizeof(int32_t) * R.n_out, cudaMemcpyDeviceToHost, st));
+    if (visit_cap && visit_log)
+        PW_CUDA(cudaMemcpyAsync(visit_log, buf + o_v, sizeof(int32_t) * std::min<int64_t>(R.n_visited, visit_cap),
+                                cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaStreamSynchronize(st));
+    out->iterations = R.c[0];
+    out->distance_computations = R.c[1];
+    out->total_visits = R.c[2];
+    out->nodes_expanded = R.c[3];
+    out->dgs_skipped = R.c[4];
+    out->inserted_total = R.c[5];
+    out->converged = R.converged;
+    out->retained = R.retained;
+    out->n_out = R.n_out;
+    out->n_visited = R.n_visited;
+    rng->state_hi = g.s_hi;
+    rng->state_lo = g.s_lo;
+    rng->inc_hi = g.i_hi;
+    rng->inc_lo = g.i_lo;
+    rng->has_uint32 = (int32_t)g.has32;
+    rng->uinteger = g.u32;
+    return 0;
 }
 
 int pw_phase_cycles(pw_shard* sh, int64_t* out8, int32_t reset) {

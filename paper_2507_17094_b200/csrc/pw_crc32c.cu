@@ -426,6 +426,7 @@ int pw_crc32c_device(const void* const* ptrs, const int64_t* lens, int32_t n, ui
         size_t cap = 0;  // sections
         uint8_t* dbuf = nullptr;
         uint8_t* hbuf = nullptr;
+        bool attr_set = false;
     };
     static DevWs ws[64];
     DevWs& W = ws[dev];
@@ -470,11 +471,10 @@ int pw_crc32c_device(const void* const* ptrs, const int64_t* lens, int32_t n, ui
     uint32_t* h_out = reinterpret_cast<uint32_t*>(W.hbuf + out_off);
     void* kbuf = W.consts;
     const size_t smem = K3_SMEM;
-    static bool attr_set = false;
-    if (!attr_set) {
+    if (!W.attr_set) {  // the opt-in shared-memory attribute is per device
         e = cudaFuncSetAttribute(crc32c_sections_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return fail(e, "smem attribute");
-        attr_set = true;
+        W.attr_set = true;
     }
     if ((e = cudaMemcpyAsync(d_secs, h, sec_bytes, cudaMemcpyHostToDevice, st)) != cudaSuccess ||
         (e = cudaMemsetAsync(d_out, 0, out_bytes, st)) != cudaSuccess)

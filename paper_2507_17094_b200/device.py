@@ -60,6 +60,22 @@ class TensorShard:
         self._finalizer = weakref.finalize(self, lib.pw_shard_destroy, h)
 
 
+def reduce_flag() -> torch.Tensor:
+    """K2's error flag in page-locked host memory: K2 writes it through the
+    unified address space (only when it fires), so checking it after the
+    results were read back costs no extra device round trip."""
+    return torch.zeros(1, dtype=torch.int32, pin_memory=True)
+
+
+def check_reduce_flag(err: torch.Tensor, device=None) -> None:
+    """Raise like pipeline.py:194 if a device-side K2 saw a query without any
+    valid candidate; clears the flag.  Synchronises the device first."""
+    torch.cuda.synchronize(device)
+    if int(err[0]):
+        err.zero_()
+        raise ValueError("cannot reduce empty candidate lists")
+
+
 def check_shard(shard: TensorShard) -> None:
     """Raise if the shard's device error flag is set (synchronises)."""
     _abi.check(_abi.load().pw_shard_check(shard.handle))
@@ -78,7 +94,7 @@ class DeviceRun:
         self.s32 = torch.empty((n_cols, 4, q), dtype=torch.int32, device=dev)
         self.s64 = torch.empty((n_cols, 6, q), dtype=torch.int64, device=dev)
         self.entries = [torch.zeros(q, dtype=torch.int32, device=dev) for _ in range(2)]
-        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.err = reduce_flag()
 
     def reset(self):
         self.shard_ids.fill_(-1)
@@ -86,7 +102,14 @@ class DeviceRun:
         self.s32.zero_()
         self.s64.zero_()
 
+    def check(self) -> None:
+        """Read and clear the K2 flag (synchronises): the device-resident
+        reduce passes a device flag instead of synchronising, so the check
+        happens where results are read back (pipeline.py:194)."""
+        check_reduce_flag(self.err, self.final_ids.device)
+
     def stats(self) -> list[dict]:
+        self.check()
         s32 = self.s32.cpu().numpy()
         s64 = self.s64.cpu().numpy()
         out = []

@@ -77,6 +77,15 @@ def dataflow_tasks(rank: int, world: int, q: int) -> list[tuple[int, int]]:
     return out
 
 
+def validate_inter(shard, n_next: int) -> None:
+    """The forwarded entries (inter_map[top1], pipeline.py:339) index the next
+    rank's shard: reject an inter_map with ids outside [0, n_next) up front
+    (they would be gather indices on the next GPU)."""
+    from . import _abi
+
+    _abi.check(_abi.load().pw_shard_validate_inter(shard.handle, int(n_next)))
+
+
 class RingSearch:
     """Device engine of one rank (one shard on this GPU)."""
 
@@ -96,6 +105,10 @@ class RingSearch:
             import torch.distributed as dist
 
             self.gloo = dist.get_backend() == "gloo"
+            sizes = [None] * world
+            dist.all_gather_object(sizes, int(shard.n))
+            if shard.has_inter:
+                validate_inter(shard, sizes[(rank + 1) % world])
 
     # ---------------------------------------------------------------- device path
     def run(self, queries, params, mode: str, timer: list | None = None) -> np.ndarray | None:
@@ -109,7 +122,9 @@ class RingSearch:
         if self.world == 1:
             dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning,
                          stream=self.stream, timer=timer)
-            return R.final_ids.cpu().numpy()
+            ids = R.final_ids.cpu().numpy()
+            R.check()
+            return ids
 
         R.reset()
         g, N = self.rank, self.world
@@ -169,7 +184,9 @@ class RingSearch:
         R.shard_ids.copy_(all_ids.permute(1, 0, 2))
         R.shard_dists.copy_(all_d.permute(1, 0, 2))
         dv.reduce(R, self.stream)
-        return R.final_ids.cpu().numpy() if self.rank == 0 else None
+        ids = R.final_ids.cpu().numpy() if self.rank == 0 else None
+        R.check()
+        return ids
 
     def last_stats(self) -> list[dict]:
         return self.run_buf.stats()
@@ -261,9 +278,11 @@ class DataflowRing:
                    dv.DevArray((N, 4, q), torch.int32), dv.DevArray((N, 6, q), torch.int64)]
         handles = [None] * world
         mine = {"inbox": self.inbox.ipc_handle(),
-                "res": [a.ipc_handle() for a in res] if res else None}
+                "res": [a.ipc_handle() for a in res] if res else None, "n": int(shard.n)}
         dist.all_gather_object(handles, mine)
         nxt = (rank + 1) % world
+        if world > 1:
+            validate_inter(shard, handles[nxt]["n"])
         self.next_inbox = self.inbox if nxt == rank else dv.DevArray((q,), torch.int64, handles[nxt]["inbox"])
         if rank == 0:
             self.res = res
@@ -273,7 +292,7 @@ class DataflowRing:
             self.res = [dv.DevArray(sh, dt, h) for (sh, dt), h in zip(shapes, handles[0]["res"])]
         self.final_ids = torch.empty((q, k), dtype=torch.int32, device=self.dev)
         self.final_dists = torch.empty((q, k), dtype=torch.float32, device=self.dev)
-        self.err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.err = dv.reduce_flag()
 
     def run(self, queries, params, mode: str, timer: list | None = None):
         """Search all queries (every rank passes the full (Q, d) device batch);
@@ -326,7 +345,9 @@ class DataflowRing:
         _abi.check(lib.pw_reduce_topk(ids.ptr, dists.ptr, self.q, N * self.k, self.k,
                                       self.final_ids.data_ptr(), self.final_dists.data_ptr(),
                                       self.err.data_ptr(), self.stream.cuda_stream))
-        return self.final_ids.cpu().numpy()
+        ids = self.final_ids.cpu().numpy()
+        dv.check_reduce_flag(self.err, self.dev)
+        return ids
 
     def last_stats(self) -> list[dict]:
         from .device import STAT_I32, STAT_I64
