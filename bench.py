@@ -304,6 +304,18 @@ def run_ours(args, cfg):
     def search(params, mode, timer=None):
         return eng.run(queries, params, mode, timer=timer)
 
+    def search_stream(params, mode, steps, timer=None):
+        """`steps` back-to-back batches: the dataflow ring enqueues them with
+        no host synchronisation in between (double-buffered slots, device-side
+        landed/done flags); the single-GPU engine returns each batch."""
+        if use_df:
+            for _ in range(steps):
+                eng.submit(queries, params, mode, timer=timer)
+            eng.sync()
+        else:
+            for _ in range(steps):
+                search(params, mode, timer=timer)
+
     # ---- operating points: per arm and DGS discard ratio, the smallest l with
     # recall@10 >= 0.95; PathWeaver keeps the (discard, l) pair with the best QPS
     def quick_ms(p, mode, reps=3):
@@ -369,8 +381,7 @@ def run_ours(args, cfg):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(steps):
-            search(p, mode, timer=timers)
+        search_stream(p, mode, steps, timer=timers)
         e1.record()
         torch.cuda.synchronize()
         if world > 1:
@@ -378,18 +389,22 @@ def run_ours(args, cfg):
         ms = e0.elapsed_time(e1)
         kern_ms = sum(a.elapsed_time(b) for a, b in timers) if with_timer else None
         launches = lib.pw_launch_count() - launches0
+        rank_kern = [kern_ms]
         if world > 1:
             t = torch.tensor([ms], device=cdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
-        return ms, kern_ms, launches
+            if with_timer:
+                rank_kern = [None] * world
+                dist.all_gather_object(rank_kern, kern_ms)
+        return ms, kern_ms, launches, rank_kern
 
     # ---- timed region (PathWeaver arm), clocks sampled meanwhile
     with ClockSampler(local) as clk:
-        ms, kern_ms, launches = timed("pathweaver", args.steps, args.warmup, with_timer=True)
+        ms, kern_ms, launches, rank_kern = timed("pathweaver", args.steps, args.warmup, with_timer=True)
     clocks = clk.summary()
     stats = eng.last_stats()
-    naive_ms, _, _ = timed("naive", max(3, args.steps // 2), 2)
+    naive_ms, _, _, _ = timed("naive", max(3, args.steps // 2), 2)
 
     # ---- roofline of the dominant kernel (beam_search_kernel).  Algorithmic
     # bytes use the reference-exact counters: with the lossy visited cache
@@ -487,6 +502,8 @@ def run_ours(args, cfg):
             "e2e": {"value": round(nq * e2e_steps / e2e_s, 1), "unit": "queries/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
+            "nvlink": nvlink_report(world, nq, k, ms / args.steps) if world > 1 else None,
+            "kernel_ms_per_rank": [round(x / args.steps, 4) for x in rank_kern] if world > 1 else None,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic_for(cfg, ops["pathweaver"]["l"], ops["pathweaver"]["discard"],
@@ -510,6 +527,24 @@ def run_ours(args, cfg):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def nvlink_report(world: int, nq: int, k: int, step_ms: float) -> dict:
+    """Bytes that cross NVLink per pipelined step of the dataflow ring, from
+    the payloads themselves: each query's entry is forwarded N-1 times as one
+    8-byte inbox word (epoch << 32 | entry; pipeline.py:339 sends 4 bytes),
+    and every rank but 0 stores its candidate-list column (k ids + k
+    distances) and one StageStats row (4 int32 + 6 int64) per query straight
+    into rank 0's buffers (no all-gather).  Reported against 900 GB/s per
+    direction per GPU."""
+    entries = 8 * (world - 1) * nq
+    columns = (world - 1) * nq * k * 8
+    stats = (world - 1) * nq * (4 * 4 + 6 * 8)
+    total = entries + columns + stats
+    per_gpu_gbs = total / world / (step_ms / 1e3) / 1e9
+    return {"bytes_per_step": int(total), "entry_bytes": int(entries), "column_bytes": int(columns),
+            "stats_bytes": int(stats), "per_gpu_gbs": round(per_gpu_gbs, 3), "peak_gbs_per_direction": 900.0,
+            "frac": round(per_gpu_gbs / 900.0, 6)}
 
 
 def traffic_for(cfg: dict, l: int, discard: float = 0.5, ghost_iter: int = 8):

@@ -203,6 +203,17 @@ int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, co
  * pw_run / pw_run_device call it for every pipelined ring.  0 or PW_EINVAL. */
 int pw_shard_validate_inter(pw_shard* shard, int64_t n_next);
 
+/* Stream-ordered cross-GPU flags for the pipelined dataflow ring (batches
+ * in flight without host synchronisation):
+ *   pw_signal  after all earlier work on `stream` (a persistent K1's peer
+ *              stores included) is visible system-wide, store `value` into
+ *              *flag (a device word, possibly a peer / IPC mapping);
+ *   pw_wait    hold `stream` until every *flags[i] >= value (flags: DEVICE
+ *              array of n <= 32 device pointers); after ~1 minute without it
+ *              sets bit 32 in *err (device int32) and releases the stream. */
+int pw_signal(uint64_t* flag, uint64_t value, void* stream);
+int pw_wait(const uint64_t* const* flags, int32_t n, uint64_t value, int32_t* err, void* stream);
+
 /* Synchronous check of a shard's device error flag (table overflow, a
  * dataflow inbox that never filled); clears it.  0 or PW_ECUDA + message. */
 int pw_shard_check(pw_shard* shard);

@@ -113,6 +113,7 @@ struct KArgs {
     int32_t lshift;         // lossy cache slot = hash32(id) >> lshift
     uint32_t* gepoch;       // per-warp search epoch (tags the spill table; no clearing)
     uint32_t* gscratch;     // per-warp global scratch for choice()
+    const uint64_t* jump;   // PCG64 jump-ahead table (kJumpMax entries, choice_floyd_warp)
     int64_t gscratch_words;
     int32_t* task_counter;
     int32_t* err;
@@ -778,7 +779,10 @@ static __device__ __noinline__ bool probe_insert(unsigned long long* gvis, uint3
 }
 
 // Lossy visited filter (tuning flag 2): a per-warp direct-mapped cache of
-// (epoch8 << 24 | id) words in global memory, small enough to stay in L2
+// 32-bit words in global memory, small enough to stay in L2.  With h =
+// hash32(id) (a bijection: odd multiplier mod 2^32) and 2^s slots, the slot
+// is h's top s bits and the word is epoch8 << 24 | h's low 32 - s bits, so
+// (slot, word) names the id exactly for any 32-bit id when s >= 8
 // (4096 slots = 16 KB per warp: measured faster than 8192 / 16384 despite
 // ~3% more re-scores -- the L2 footprint matters).  One round trip, no atomics: every miss is
 // stored (overwrites allowed) and scored.  Results stay identical to the
@@ -796,8 +800,9 @@ static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S
     uint32_t* tab = reinterpret_cast<uint32_t*>(S.gvis);
     uint32_t* vs = reinterpret_cast<uint32_t*>(S.ckey);
     const uint32_t tag = S.epoch << 24;
-#pragma unroll 1
+    const uint32_t lmask = (1u << A.lshift) - 1u;  // low 32 - s bits of h
     const uint64_t keep = l2_evict_last_policy();
+#pragma unroll 1
     for (int t = lane; t < nb; t += 32) cp_async4_keep(vs + t, tab + (hash32((uint32_t)S.newl[t]) >> A.lshift), keep);
     cp_commit();
     cp_wait<0>();
@@ -807,8 +812,9 @@ static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S
     for (int base = 0; base < nb; base += 32) {
         const int t = base + (int)lane;
         const uint32_t id = t < nb ? (uint32_t)S.newl[t] : 0u;
-        const bool fresh = t < nb && vs[t] != (tag | id);
-        if (fresh) st_keep(&tab[hash32(id) >> A.lshift], tag | id, keep);
+        const uint32_t h = hash32(id);
+        const bool fresh = t < nb && vs[t] != (tag | (h & lmask));
+        if (fresh) st_keep(&tab[h >> A.lshift], tag | (h & lmask), keep);
         const unsigned b = __ballot_sync(0xffffffffu, fresh);
         if (fresh) S.newl[cnt + __popc(b & lanemask_lt())] = (int32_t)id;
         cnt += __popc(b);
@@ -1079,15 +1085,27 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     // ckey[0..s): the survivors (keys below the l-th key), filtered by score_rows
     if (s == 0) return 0;
     if (s <= 32) {
-        uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
-        x = warp_sort_u64(x);
-        if ((int)lane < s) S.ckey[lane] = x;
+        // rank by counting smaller keys (keys are unique): s broadcast loads
+        // per lane instead of a 15-stage shuffle network
+        const uint64_t x = (int)lane < s ? S.ckey[lane] : ~0ull;
+        int rank = 0;
+#pragma unroll 4
+        for (int o = 0; o < s; o++) rank += S.ckey[o] < x;
+        __syncwarp();
+        if ((int)lane < s) S.ckey[rank] = x;
     } else if (s <= 64) {
-        uint64_t x0 = S.ckey[lane];
-        uint64_t x1 = 32 + (int)lane < s ? S.ckey[32 + lane] : ~0ull;
-        warp_sort2_u64(x0, x1);
-        S.ckey[lane] = x0;
-        if (32 + (int)lane < s) S.ckey[32 + lane] = x1;
+        const uint64_t x0 = S.ckey[lane];
+        const uint64_t x1 = 32 + (int)lane < s ? S.ckey[32 + lane] : ~0ull;
+        int r0 = 0, r1 = 0;
+#pragma unroll 4
+        for (int o = 0; o < s; o++) {
+            const uint64_t y = S.ckey[o];
+            r0 += y < x0;
+            r1 += y < x1;
+        }
+        __syncwarp();
+        S.ckey[r0] = x0;
+        if (32 + (int)lane < s) S.ckey[r1] = x1;
     } else {
         sort_survivors_smem(S.ckey, s);
     }
@@ -1099,6 +1117,17 @@ static __device__ int merge_queue(const KArgs& A, WarpState& S, const SearchCfg&
     while (qstep <= qlen) qstep <<= 1;
     qstep >>= 1;
     bool dup = false;
+    if (s <= 32) {  // the common case: one search per lane
+        if ((int)lane < s) {
+            const uint64_t k0 = S.ckey[lane];
+            int p0 = 0;
+            for (int st = qstep; st > 0; st >>= 1)
+                if (p0 + st <= qlen && qk[p0 + st - 1] < k0) p0 += st;
+            const bool d0 = p0 < qlen && qk[p0] == k0;
+            dup = d0;
+            ppos[lane] = d0 ? -1 : p0;
+        }
+    } else
     for (int i0 = lane; i0 < s; i0 += 64) {
         const int i1 = i0 + 32;
         const uint64_t k0 = S.ckey[i0];
@@ -1396,6 +1425,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                             }
                         });
             if (WC > 0 && j <= 32) {
+                const unsigned valid = __ballot_sync(0xffffffffu, (int)lane < j);
                 // per parent: query direction bits pack(q >= x_parent) as W
                 // ballots (direction.py:53-59), matching count per slot
                 // (lane = slot, :62-69), one warp bitonic sort on (count desc,
@@ -1426,23 +1456,22 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                         c = d - diff;
                     }
                     // rank = #slots with a larger count + #equal-count slots
-                    // before this one: bit-serial ballot radix over count bits
-                    constexpr int NB = D >= 512 ? 10 : D >= 256 ? 9 : D >= 128 ? 8 : D >= 64 ? 7 : 6;
-                    const unsigned valid = __ballot_sync(0xffffffffu, (int)lane < j);
-                    unsigned eq = valid;
-                    int gt = 0;
+                    // before this one: bit-serial ballot radix over the count
+                    // bits, MSB first.  eq = slots equal to mine on the bits
+                    // seen so far; gtm collects the slots that first differ
+                    // from mine with a 1 where I have a 0 (larger counts).
+                    // Masks, not running counts: one popc at the end.
+                    constexpr int NB = D >= 1024 ? 11 : D >= 512 ? 10 : D >= 256 ? 9 : D >= 128 ? 8 : D >= 64 ? 7 : 6;
+                    unsigned eq = valid, gtm = 0u;
 #pragma unroll
-                    for (int b = (D >= 1024 ? 11 : NB) - 1; b >= 0; b--) {
-                        const bool mine = (c >> b) & 1;
-                        const unsigned B = __ballot_sync(0xffffffffu, mine) & valid;
-                        if (mine) {
-                            eq &= B;
-                        } else {
-                            gt += __popc(eq & B);
-                            eq &= ~B;
-                        }
+                    for (int b = NB - 1; b >= 0; b--) {
+                        const unsigned m = 0u - (((unsigned)c >> b) & 1u);  // all ones iff my bit b is set
+                        const unsigned B = __ballot_sync(0xffffffffu, m != 0u);
+                        const unsigned t = eq & B;
+                        gtm |= t & ~m;
+                        eq &= ~(B ^ m);
                     }
-                    const int rank = gt + __popc(eq & lanemask_lt());
+                    const int rank = __popc(gtm) + __popc(eq & lanemask_lt());
                     if ((int)lane < j && rank < nsel)
                         S.cand[(pg + pi) * nsel + rank] = craw[(pg + pi) * j + lane];
                 }
@@ -1558,8 +1587,19 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     int nb = dedup_ordered(A, S, S.cand, ns, C.want, S.newl, &nuniq);
     if (fill_random && nb < C.want) {
         int32_t* ch = S.cand;
-        if (lane == 0) {
-            const uint32_t pop = (uint32_t)G.n, size = (uint32_t)C.want;
+        const uint32_t pop = (uint32_t)G.n, size = (uint32_t)C.want;
+        // warp-parallel Floyd when exact (rare rejections / repeats fall back
+        // to the serial restatement); the draw order matters only when seeds
+        // precede the fill (the first want - nb new values are kept) or the
+        // visit log records it
+        bool done = false;
+        if (size <= (uint32_t)kJumpMax && pop > size && !choice_uses_tail(pop, size)) {
+            const Pcg64 r = choice_floyd_warp(rng, pop, size, nb > 0 || C.log, A.jump,
+                                              A.CB > 64 ? reinterpret_cast<uint32_t*>(S.ckey) : S.gscr, ch);
+            done = r.has32 < 2u;
+            if (done) rng = r;
+        }
+        if (!done && lane == 0) {
             if (choice_uses_tail(pop, size)) {
                 uint32_t cap = 1;
                 while (cap < 4u * size + 8u) cap <<= 1;

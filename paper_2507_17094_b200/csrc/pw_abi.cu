@@ -141,7 +141,27 @@ struct DevInfo {
     int sms = 0;
     int smem_optin = 0;
     bool attr_set = false;
+    uint64_t* jump = nullptr;  // PCG64 jump-ahead table on this device
 };
+
+// {A^k, A^(k-1) + ... + A + 1} mod 2^128 for k = 1..kJumpMax (numpy PCG64's
+// 128-bit LCG multiplier A), as {M_hi, M_lo, S_hi, S_lo} per k.
+std::vector<uint64_t> pcg_jump_table() {
+    typedef unsigned __int128 u128;
+    const u128 A = ((u128)2549297995355413924ULL << 64) | 4865540595714422341ULL;
+    std::vector<uint64_t> t(4 * kJumpMax);
+    u128 M = 1, S = 0;
+    for (int k = 1; k <= kJumpMax; k++) {
+        S = S + M;  // S_k = S_(k-1) + A^(k-1)
+        M = M * A;  // A^k
+        uint64_t* e = &t[4 * (k - 1)];
+        e[0] = (uint64_t)(M >> 64);
+        e[1] = (uint64_t)M;
+        e[2] = (uint64_t)(S >> 64);
+        e[3] = (uint64_t)S;
+    }
+    return t;
+}
 std::mutex g_dev_mu;
 DevInfo g_dev[64];
 
@@ -151,6 +171,20 @@ int dev_info(int dev, DevInfo** out) {
     if (I.sms == 0) {
         PW_CUDA(cudaDeviceGetAttribute(&I.sms, cudaDevAttrMultiProcessorCount, dev));
         PW_CUDA(cudaDeviceGetAttribute(&I.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    }
+    // per-device state below is created on `dev` (the caller's current
+    // device is restored on return)
+    int cur = dev;
+    PW_CUDA(cudaGetDevice(&cur));
+    struct Restore {
+        int d;
+        ~Restore() { cudaSetDevice(d); }
+    } restore{cur};
+    if (cur != dev) PW_CUDA(cudaSetDevice(dev));
+    if (!I.jump) {
+        const std::vector<uint64_t> t = pcg_jump_table();
+        PW_CUDA(cudaMalloc(&I.jump, t.size() * sizeof(uint64_t)));
+        PW_CUDA(cudaMemcpy(I.jump, t.data(), t.size() * sizeof(uint64_t), cudaMemcpyHostToDevice));
     }
     if (!I.attr_set) {
         PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_0(),
@@ -317,6 +351,33 @@ __global__ void reduce_topk_kernel(const int32_t* __restrict__ ids, const float*
         }
         __syncwarp();
     }
+}
+
+// Cross-GPU ordering for the pipelined dataflow ring (ring.DataflowRing):
+// signal_kernel publishes `value` into a (peer-mapped) flag after everything
+// earlier on its stream -- the persistent K1's stores into other GPUs'
+// buffers included -- is visible system-wide; wait_kernel holds its stream
+// until every flag reaches `value` (bounded: a peer that never signals sets
+// err instead of hanging the GPU).
+__global__ void signal_kernel(unsigned long long* flag, unsigned long long value) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+    st_release_sys(flag, value);
+}
+__global__ void wait_kernel(const unsigned long long* const* flags, int32_t n, unsigned long long value,
+                            int32_t* err) {
+    const int i = threadIdx.x;
+    if (i < n) {
+        for (uint32_t spin = 0;; spin++) {
+            if (ld_acquire_sys(flags[i]) >= value) break;
+            if (spin > (1u << 26)) {
+                atomicOr(err, 32);
+                break;
+            }
+            __nanosleep(512);
+        }
+    }
+    __syncthreads();
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
 
 // Test hook: exact squared L2 of rows[ids] vs query (data.py:70-79).
@@ -629,13 +690,15 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // the spill triggers when (smem entries + batch) > vis_limit, so a table is
     // needed whenever bound + CB can exceed it; it holds <= bound entries
     int64_t gsz = (specialised || bound + cb > A.vis_limit) ? next_pow2(2 * bound + 2) : 1;
-    // lossy visited cache (tuning flag 2): u32 (epoch8 << 24 | id) slots, so
-    // ids must fit 24 bits; never with log_visits (the log lists exact visits)
-    const bool lossy = tun && (tun->flags & 2) && std::max<int64_t>(sh->n, sh->gn) < (1 << 24) &&
-                       !p.log_visits;
+    // lossy visited cache (tuning flag 2): u32 slots holding epoch8 << 24 |
+    // the low 32 - s bits of hash32(id) (any shard size: >= 2^8 slots make
+    // slot + word name the id exactly); never with log_visits (the log lists
+    // exact visits)
+    const bool lossy = tun && (tun->flags & 2) && !p.log_visits;
     A.lossy = lossy ? 1 : 0;
     if (lossy) {
-        const int64_t slots = std::max<int64_t>(64, next_pow2(tun->visited_slots > 0 ? tun->visited_slots : 4096));
+        const int64_t slots = std::min<int64_t>(
+            1ll << 24, std::max<int64_t>(256, next_pow2(tun->visited_slots > 0 ? tun->visited_slots : 4096)));
         int lg = 0;
         while ((1ll << lg) < slots) lg++;
         A.lshift = 32 - lg;
@@ -686,6 +749,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     A.gvis = sh->gvis;
     A.gepoch = sh->gepoch;
     A.gscratch = sh->gscr;
+    A.jump = I->jump;
     A.gscratch_words = scr;
     A.task_counter = sh->counter;
     A.err = sh->counter + 1;
@@ -902,6 +966,23 @@ int pw_shard_validate_inter(pw_shard* sh, int64_t n_next) {
     return 0;
 }
 
+int pw_signal(uint64_t* flag, uint64_t value, void* stream) {
+    if (!flag) return set_err(PW_EINVAL, "null argument");
+    signal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(flag), value);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
+}
+
+int pw_wait(const uint64_t* const* flags, int32_t n, uint64_t value, int32_t* err, void* stream) {
+    if (!flags || !err || n < 1 || n > 32) return set_err(PW_EINVAL, "pw_wait needs 1..32 flags and an err flag");
+    wait_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long* const*>(flags), n,
+                                                    value, err);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
+}
+
 int pw_shard_check(pw_shard* sh) {
     if (!sh) return set_err(PW_EINVAL, "null argument");
     if (!sh->counter) return 0;
@@ -983,57 +1064,22 @@ int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q
     return 0;
 }
 
-int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
-                  const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
-                  int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
-                  int32_t* stats_i32, int64_t* stats_i64, int32_t* entries_a, int32_t* entries_b,
-                  void* stream) {
-    if (N < 1 || !shards) return set_err(PW_EINVAL, "need at least one shard");
-    cudaStream_t st = (cudaStream_t)stream;
-    const int64_t k = params->k;
-    PW_CUDA(cudaMemsetAsync(shard_ids, 0xFF, sizeof(int32_t) * q * N * k, st));  // -1 padding
-    int rc = pw_fill_inf(shard_dists, q * N * k, st);                              // +inf padding
-    if (rc) return rc;
-    PW_CUDA(cudaMemsetAsync(stats_i32, 0, sizeof(int32_t) * 4 * q * N, st));
-    PW_CUDA(cudaMemsetAsync(stats_i64, 0, sizeof(int64_t) * 6 * q * N, st));
-    if (mode == PW_MODE_BASELINE) {
-        for (int s = 0; s < N; s++) {  // pipeline.py:288-297
-            rc = pw_search_stage(shards[s], params, tuning, queries, 0, q, s, nullptr, nullptr,
-                                 shard_ids, shard_dists, N, s, stats_i32 + (int64_t)s * 4 * q,
-                                 stats_i64 + (int64_t)s * 6 * q, q, st);
-            if (rc) return rc;
-        }
-    } else {
-        if (N > 1)
-            for (int s = 0; s < N; s++)  // forwarded entries index shard s+1 (pipeline.py:339)
-                if ((rc = pw_shard_validate_inter(shards[s], shards[(s + 1) % N]->n))) return rc;
-        std::vector<int64_t> lo(N + 1, 0);  // np.array_split(arange(Q), N)
-        for (int c = 0; c < N; c++) lo[c + 1] = lo[c] + q / N + (c < q % N ? 1 : 0);
-        int32_t* ein = entries_a;
-        int32_t* eout = entries_b;
-        for (int stage = 0; stage < N; stage++) {  // pipeline.py:344-347
-            for (int c = 0; c < N; c++) {
-                int shard = (c + stage) % N;
-                rc = pw_search_stage(shards[shard], params, tuning, queries, lo[c], lo[c + 1] - lo[c],
-                                     stage, stage > 0 ? ein : nullptr,
-                                     stage < N - 1 ? eout : nullptr, shard_ids, shard_dists, N, shard,
-                                     stats_i32 + (int64_t)stage * 4 * q,
-                                     stats_i64 + (int64_t)stage * 6 * q, q, st);
-                if (rc) return rc;
-            }
-            std::swap(ein, eout);
-        }
-    }
-    return 0;
-}
-
-// Grow-only per-device workspace of pw_run (no allocation inside a steady
-// stream of calls, so end-to-end timings measure copies + kernels only).
+// Grow-only per-device workspace of the host entry points (no allocation
+// inside a steady stream of calls, so end-to-end timings measure copies +
+// kernels only).  Its mutex serialises every host call that launches on the
+// device's shards (pw_run, pw_run_device, pw_search_one): a shard's launch
+// workspace (task counter, visited tables) belongs to one launch at a time.
 struct RunWs {
     std::mutex mu;
     cudaStream_t st = nullptr;
     char* buf = nullptr;
     size_t cap = 0;
+    // logical-shard dataflow ring: one stream per shard, inboxes, run tag
+    cudaStream_t ring[8] = {};
+    cudaEvent_t ev[9] = {};
+    uint64_t* inbox = nullptr;
+    size_t inbox_cap = 0;  // u64 words
+    uint32_t epoch = 0;
 };
 RunWs g_ws[64];
 
@@ -1049,6 +1095,120 @@ int ws_reserve(RunWs& W, size_t bytes) {
     PW_CUDA(cudaMalloc(&W.buf, bytes));
     W.cap = bytes;
     return 0;
+}
+
+// Pipelined path extension over N logical shards of one device as the
+// dataflow ring (pipeline.py:308-347): N persistent K1 launches on N
+// streams, each capped to SMs/N CTAs so all are resident together; shard g
+// runs its (stage, query) tasks stage-major and hands each entry to shard
+// g+1 through a device inbox -- no stage barriers, one launch per shard
+// instead of N x N stage launches.  Stream-ordered after `st`; `st` waits
+// for all of them.
+int run_dataflow_local(RunWs& W, pw_shard* const* shards, int32_t N, const pw_params* params,
+                       const pw_tuning* tuning, const float* queries, int64_t q, int32_t* shard_ids,
+                       float* shard_dists, int32_t* stats_i32, int64_t* stats_i64, cudaStream_t st) {
+    for (int g = 0; g < N; g++) {
+        if (!W.ring[g]) PW_CUDA(cudaStreamCreateWithFlags(&W.ring[g], cudaStreamNonBlocking));
+        if (!W.ev[g]) PW_CUDA(cudaEventCreateWithFlags(&W.ev[g], cudaEventDisableTiming));
+    }
+    if (!W.ev[8]) PW_CUDA(cudaEventCreateWithFlags(&W.ev[8], cudaEventDisableTiming));
+    const size_t words = (size_t)N * (size_t)q;
+    if (W.inbox_cap < words) {
+        PW_CUDA(cudaStreamSynchronize(st));
+        if (W.inbox) cudaFree(W.inbox);
+        W.inbox = nullptr;
+        W.inbox_cap = 0;
+        PW_CUDA(cudaMalloc(&W.inbox, words * sizeof(uint64_t)));
+        PW_CUDA(cudaMemset(W.inbox, 0, words * sizeof(uint64_t)));  // tag 0 is never a run's
+        W.inbox_cap = words;
+        W.epoch = 0;
+    }
+    if (++W.epoch == 0) {  // 2^32 runs: re-zero so no stale word can match
+        PW_CUDA(cudaStreamSynchronize(st));
+        PW_CUDA(cudaMemset(W.inbox, 0, W.inbox_cap * sizeof(uint64_t)));
+        W.epoch = 1;
+    }
+    DevInfo* I;
+    int rc = dev_info(shards[0]->device, &I);
+    if (rc) return rc;
+    const int sm_limit = std::max(1, I->sms / N);
+    PW_CUDA(cudaEventRecord(W.ev[8], st));
+    for (int g = 0; g < N; g++) {
+        PW_CUDA(cudaStreamWaitEvent(W.ring[g], W.ev[8], 0));
+        rc = pw_search_dataflow(shards[g], params, tuning, queries, q, g, N, W.epoch,
+                                W.inbox + (size_t)g * q, W.inbox + (size_t)((g + 1) % N) * q, shard_ids,
+                                shard_dists, stats_i32, stats_i64, sm_limit, W.ring[g]);
+        if (rc) return rc;
+        PW_CUDA(cudaEventRecord(W.ev[g], W.ring[g]));
+    }
+    for (int g = 0; g < N; g++) PW_CUDA(cudaStreamWaitEvent(st, W.ev[g], 0));
+    return 0;
+}
+
+int run_device_impl(RunWs& W, pw_shard* const* shards, int32_t N, const pw_params* params,
+                    const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
+                    int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
+                    int32_t* stats_i32, int64_t* stats_i64, int32_t* entries_a, int32_t* entries_b,
+                    int32_t* err_dev, cudaStream_t st) {
+    if (N < 1 || !shards) return set_err(PW_EINVAL, "need at least one shard");
+    int rc = validate_params(*params);
+    if (rc) return rc;
+    const int64_t k = params->k;
+    PW_CUDA(cudaMemsetAsync(shard_ids, 0xFF, sizeof(int32_t) * q * N * k, st));  // -1 padding
+    if ((rc = pw_fill_inf(shard_dists, q * N * k, st))) return rc;               // +inf padding
+    PW_CUDA(cudaMemsetAsync(stats_i32, 0, sizeof(int32_t) * 4 * q * N, st));
+    PW_CUDA(cudaMemsetAsync(stats_i64, 0, sizeof(int64_t) * 6 * q * N, st));
+    if (mode == PW_MODE_BASELINE) {
+        for (int s = 0; s < N; s++) {  // pipeline.py:288-297
+            rc = pw_search_stage(shards[s], params, tuning, queries, 0, q, s, nullptr, nullptr,
+                                 shard_ids, shard_dists, N, s, stats_i32 + (int64_t)s * 4 * q,
+                                 stats_i64 + (int64_t)s * 6 * q, q, st);
+            if (rc) return rc;
+        }
+    } else {
+        if (N > 1)
+            for (int s = 0; s < N; s++)  // forwarded entries index shard s+1 (pipeline.py:339)
+                if ((rc = pw_shard_validate_inter(shards[s], shards[(s + 1) % N]->n))) return rc;
+        if (N > 1 && N <= 8 && q >= N) {
+            rc = run_dataflow_local(W, shards, N, params, tuning, queries, q, shard_ids, shard_dists, stats_i32,
+                                    stats_i64, st);
+            if (rc) return rc;
+        } else {
+            // stage-synchronous schedule (N = 1, or more shards than the
+            // dataflow task map holds): chunk c at stage s on shard (c+s)%N
+            std::vector<int64_t> lo(N + 1, 0);  // np.array_split(arange(Q), N)
+            for (int c = 0; c < N; c++) lo[c + 1] = lo[c] + q / N + (c < q % N ? 1 : 0);
+            int32_t* ein = entries_a;
+            int32_t* eout = entries_b;
+            for (int stage = 0; stage < N; stage++) {  // pipeline.py:344-347
+                for (int c = 0; c < N; c++) {
+                    int shard = (c + stage) % N;
+                    rc = pw_search_stage(shards[shard], params, tuning, queries, lo[c], lo[c + 1] - lo[c],
+                                         stage, stage > 0 ? ein : nullptr, stage < N - 1 ? eout : nullptr,
+                                         shard_ids, shard_dists, N, shard, stats_i32 + (int64_t)stage * 4 * q,
+                                         stats_i64 + (int64_t)stage * 6 * q, q, st);
+                    if (rc) return rc;
+                }
+                std::swap(ein, eout);
+            }
+        }
+    }
+    return pw_reduce_topk(shard_ids, shard_dists, q, (int32_t)(N * k), (int32_t)k, final_ids, final_dists,
+                          err_dev, st);
+}
+
+int pw_run_device(pw_shard* const* shards, int32_t N, const pw_params* params,
+                  const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
+                  int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,
+                  int32_t* stats_i32, int64_t* stats_i64, int32_t* entries_a, int32_t* entries_b,
+                  void* stream) {
+    if (N < 1 || !shards) return set_err(PW_EINVAL, "need at least one shard");
+    PW_CUDA(cudaSetDevice(shards[0]->device));
+    RunWs& W = g_ws[shards[0]->device];
+    std::lock_guard<std::mutex> lk(W.mu);
+    // NULL err: K2 synchronises and reports empty lists itself
+    return run_device_impl(W, shards, N, params, tuning, queries, q, mode, shard_ids, shard_dists, final_ids,
+                           final_dists, stats_i32, stats_i64, entries_a, entries_b, nullptr, (cudaStream_t)stream);
 }
 
 int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw_tuning* tuning,
@@ -1093,10 +1253,9 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     int32_t* err = (int32_t*)(b + o_err);
     PW_CUDA(cudaMemcpyAsync(dq, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
     PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
-    rc = pw_run_device(shards, N, params, tuning, dq, q, mode, sid, sd, fid, fd, s32, s64,
-                       (int32_t*)(b + o_ea), (int32_t*)(b + o_eb), st);
+    rc = run_device_impl(W, shards, N, params, tuning, dq, q, mode, sid, sd, fid, fd, s32, s64,
+                         (int32_t*)(b + o_ea), (int32_t*)(b + o_eb), err, st);
     if (rc) return rc;
-    if ((rc = pw_reduce_topk(sid, sd, q, (int32_t)(N * k), (int32_t)k, fid, fd, err, st))) return rc;
     int32_t herr = 0;
     PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(shard_dists, sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));

@@ -243,6 +243,154 @@ PW_HD_COLD Pcg64 choice_tail(Pcg64 g, uint32_t pop, uint32_t size, uint32_t* key
 
 PW_HD bool choice_uses_tail(uint32_t pop, uint32_t size) { return pop > 10000u && size > pop / 50u; }
 
+#ifdef __CUDACC__
+// ---- warp-parallel Floyd choice (jump-ahead PCG64)
+//
+// state_k (after k steps of state = A * state + inc) = M_k * s + S_k * inc
+// with M_k = A^k and S_k = A^(k-1) + ... + A + 1 (mod 2^128): one 128-bit
+// multiply-add per lane replaces a chain of k dependent steps.  `jump` holds
+// k = 1..kJumpMax as {M_hi, M_lo, S_hi, S_lo} (pw_abi.cu builds it).
+constexpr int kJumpMax = 64;
+
+__device__ __forceinline__ void mul_lo128(uint64_t ah, uint64_t al, uint64_t bh, uint64_t bl, uint64_t& rh,
+                                          uint64_t& rl) {
+    rl = al * bl;
+    rh = __umul64hi(al, bl) + al * bh + ah * bl;
+}
+
+__device__ __forceinline__ uint64_t xsl_rr(uint64_t hi, uint64_t lo) {
+    const uint64_t x = hi ^ lo;
+    const unsigned rot = (unsigned)(hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+
+// Lemire draw of bounded_u32(g, rng) from one 32-bit value u: the result, or
+// `rej` set when numpy would reject u and draw again.
+__device__ __forceinline__ uint32_t lemire_once(uint32_t u, uint32_t rng, bool& rej) {
+    const uint32_t excl = rng + 1u;
+    const uint64_t m = (uint64_t)u * excl;
+    const uint32_t left = (uint32_t)m;
+    rej = left < excl && left < (0xFFFFFFFFu - rng) % excl;
+    return (uint32_t)(m >> 32);
+}
+
+// Generator.choice(pop, size, replace=False) in its Floyd branch, all lanes
+// of the warp, bit-exact with choice_floyd.  The 2*size-1 32-bit draws
+// (size Floyd values, size-1 for _shuffle_int) come from jump-ahead outputs
+// computed in parallel; the result is speculative on the two rare events
+// that make numpy's draw sequence data-dependent -- a Lemire rejection (an
+// extra draw) and a repeated Floyd value (the j substitution) -- and on
+// either one the warp returns g unchanged but for has32 |= 2 (not handled:
+// the caller runs the serial restatement).  Otherwise returns the advanced
+// generator.  order = false skips the swaps of the final shuffle
+// (callers that use the result as a set) but g still advances past its draws.
+// buf: >= 128 u32 of warp-private scratch; requires 1 <= size <= 64,
+// pop > size and the Floyd branch (!choice_uses_tail).
+static __device__ __noinline__ Pcg64 choice_floyd_warp(Pcg64 g, uint32_t pop, uint32_t size, bool order, const uint64_t* jump,
+                                  uint32_t* buf, int32_t* out) {
+    const unsigned lane = threadIdx.x & 31u;
+    const uint32_t K = 2u * size - 1u;               // 32-bit draws
+    const uint32_t off = g.has32;                    // draw 0 is the buffered half
+    const uint32_t n64 = (K - off + 1u) / 2u;        // 64-bit outputs consumed
+    // outputs k = lane, lane + 32 -> buf as little-endian u64 (low half first)
+    uint64_t fin_hi = 0, fin_lo = 0;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const uint32_t k = lane + 32u * r;
+        if (k < n64) {
+            const uint64_t* J = jump + 4 * (size_t)k;  // entry k+1
+            uint64_t mh, ml, ah, al;
+            mul_lo128(__ldg(J), __ldg(J + 1), g.s_hi, g.s_lo, mh, ml);
+            mul_lo128(__ldg(J + 2), __ldg(J + 3), g.i_hi, g.i_lo, ah, al);
+            const uint64_t lo = ml + al;
+            const uint64_t hi = mh + ah + (lo < ml ? 1u : 0u);
+            reinterpret_cast<uint64_t*>(buf)[k] = xsl_rr(hi, lo);
+            if (k == n64 - 1u) {
+                fin_hi = hi;
+                fin_lo = lo;
+            }
+        }
+    }
+    __syncwarp();
+    uint32_t v[4];
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const uint32_t t = lane + 32u * r;
+        v[r] = 0;
+        if (t < K) {
+            const uint32_t u = (off && t == 0) ? g.u32 : buf[t - off];
+            const uint32_t rng = t < size ? pop - size + t : 2u * size - 1u - t;
+            bool rej;
+            v[r] = lemire_once(u, rng, rej);
+            bad |= rej;
+        }
+    }
+    const uint32_t last_hi = n64 ? buf[2u * n64 - 1u] : g.u32;
+    if (__any_sync(0xffffffffu, bad)) {
+        g.has32 |= 2u;
+        return g;
+    }
+    __syncwarp();
+    // repeated Floyd values (numpy would substitute j): 128-slot hash in buf
+    for (uint32_t i = lane; i < 128u; i += 32u) buf[i] = 0xFFFFFFFFu;
+    __syncwarp();
+    bool dup = false;
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const uint32_t t = lane + 32u * r;
+        if (t < size) {
+            uint32_t h = (v[r] * 0x9E3779B1u) >> 25;
+            for (;;) {
+                const uint32_t o = atomicCAS(&buf[h], 0xFFFFFFFFu, v[r]);
+                if (o == 0xFFFFFFFFu) break;
+                if (o == v[r]) {
+                    dup = true;
+                    break;
+                }
+                h = (h + 1u) & 127u;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, dup)) {
+        g.has32 |= 2u;
+        return g;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const uint32_t t = lane + 32u * r;
+        if (t < size) out[t] = (int32_t)v[r];
+    }
+    if (order) {
+        // _shuffle_int(size, 1): swap out[i] with out[draw] for i = size-1..1
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+            const uint32_t t = lane + 32u * r;
+            if (t >= size && t < K) buf[t - size] = v[r];
+        }
+        __syncwarp();
+        if (lane == 0)
+            for (uint32_t i = size - 1u; i >= 1u; i--) {
+                const uint32_t jj = buf[size - 1u - i];
+                const int32_t x = out[jj];
+                out[jj] = out[i];
+                out[i] = x;
+            }
+    }
+    __syncwarp();
+    // generator after the last consumed draw (broadcast from its lane)
+    if (n64) {
+        const int src = (int)((n64 - 1u) & 31u);
+        g.s_hi = __shfl_sync(0xffffffffu, fin_hi, src);
+        g.s_lo = __shfl_sync(0xffffffffu, fin_lo, src);
+        g.u32 = last_hi;
+    }
+    g.has32 = ((K - off) & 1u) ? 1u : 0u;
+    return g;
+}
+#endif
+
 // Generator.permutation(n) into out[n]
 PW_HD_COLD Pcg64 permutation(Pcg64 g, uint32_t n, int32_t* out) {
     for (uint32_t i = 0; i < n; i++) out[i] = (int32_t)i;

@@ -276,10 +276,12 @@ class LocalDataflow:
 def algorithmic_bytes(stats: list[dict], params, d: int, j: int, j_g: int, esize: int = 4,
                       seeded_stages: set | None = None) -> float:
     """Gather bytes the search path must read (per query summed):
-    DC*d*s_e + (E + S)*j*4 + E_ghost*j_g*4 + P*(j*W*4 + d*s_e)
+    DC*d*s_e + (E + S)*j*4 + E_ghost*j_g*4 + P*j*W*4
     with P = pruned expansions = dgs_skipped / (j - n_keep) (each pruned parent
-    reads its direction row and its own vector, search.py:257-258) and S = 1
-    per neighbour-seeded search (adj[entry] read, pipeline.py:231)."""
+    reads its direction row, search.py:258) and S = 1 per neighbour-seeded
+    search (adj[entry] read, pipeline.py:231).  Kernel-side re-reads (a
+    parent's own vector for the DGS query bits, lossy-cache re-scores) are
+    excluded, as §8(d) specifies."""
     W = (d + 31) // 32
     n_keep = max(1, int((1.0 - params.discard_ratio) * j + 0.5))
     total = 0.0
@@ -293,5 +295,5 @@ def algorithmic_bytes(stats: list[dict], params, d: int, j: int, j_g: int, esize
             seeded = float((st["ghost_iterations"] > 0).sum())
             if seeded_stages and s in seeded_stages:
                 seeded = float(len(st["iterations"]))
-        total += dc * d * esize + (e + seeded) * j * 4 + eg * j_g * 4 + pruned * (j * W * 4 + d * esize)
+        total += dc * d * esize + (e + seeded) * j * 4 + eg * j_g * 4 + pruned * j * W * 4
     return total

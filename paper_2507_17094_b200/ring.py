@@ -243,22 +243,36 @@ class RingSearch:
 
 class DataflowRing:
     """One shard per GPU, pipelined path extension WITHOUT stage barriers
-    (pw_search_dataflow): each rank runs one persistent K1 over all its
-    (stage, query) tasks; a finished stage-s search stores its entry
-    (inter_map[top1], pipeline.py:339) straight into rank g+1's inbox -- a
-    CUDA IPC peer mapping, so the 8-byte store travels over NVLink -- and
-    writes its candidate-list column and counters straight into rank 0's
-    result buffers.  The only host synchronisation per run is one barrier
-    before (rank 0's buffers are free again) and one after (all columns
-    landed); rank 0 then runs K2.  Baseline mode uses the same peer outputs
-    with one pw_search_stage launch per rank (no exchange at all).
+    (pw_search_dataflow) and without host synchronisation between batches.
 
-    torch.distributed (NCCL or gloo) only carries the 64-byte IPC handles
-    and the barriers.  Ranks may share a GPU (tests): pass sm_limit so every
+    Each rank runs one persistent K1 per batch over all its (stage, query)
+    tasks; a finished stage-s search stores its entry (inter_map[top1],
+    pipeline.py:339) straight into rank g+1's inbox -- a CUDA IPC peer
+    mapping, so the 8-byte store travels over NVLink -- and writes its
+    candidate-list column and counters straight into rank 0's result
+    buffers.  Batches are double-buffered (``depth`` slots of inboxes and of
+    rank 0's result buffers) and ordered on the device only:
+
+    * every rank, after its K1 of batch e: ``pw_signal(landed[g][slot], e)``
+      (a word in rank 0's memory);
+    * rank 0: ``pw_wait(landed[*][slot] >= e)``, then K2 into the slot's
+      final lists;
+    * before a slot is reused by batch e + depth, rank 0 resets its buffers
+      on its stream (after that slot's K2) and ``pw_signal(done[slot], e)``;
+      every other rank ``pw_wait(done[slot] >= e)`` before its K1 of batch
+      e + depth -- which also proves every rank consumed the slot's inboxes.
+
+    ``submit`` only enqueues; ``result`` waits for one batch (rank 0).  So a
+    stream of batches keeps every GPU busy: rank g starts batch e+1 while
+    rank 0 still reduces batch e.  Baseline mode (naive sharding) uses the
+    same slots with one pw_search_stage launch per rank.
+
+    torch.distributed (NCCL or gloo) only carries the 64-byte IPC handles at
+    construction.  Ranks may share a GPU (tests): pass sm_limit so every
     rank's persistent kernel stays resident."""
 
     def __init__(self, shard, q: int, k: int, rank: int, world: int, device, tuning=None,
-                 sm_limit: int = 0):
+                 sm_limit: int = 0, depth: int = 2):
         import torch
         import torch.distributed as dist
 
@@ -269,52 +283,84 @@ class DataflowRing:
         self.dev = torch.device(device)
         self.stream = torch.cuda.current_stream(self.dev)
         self.sm_limit = sm_limit
+        self.depth = depth
         self.epoch = 0
         N = world
-        self.inbox = dv.DevArray((q,), torch.int64)
-        res = None
+        self.inbox = dv.DevArray((depth, q), torch.int64)
+        res = flags = None
         if rank == 0:
-            res = [dv.DevArray((q, N, k), torch.int32), dv.DevArray((q, N, k), torch.float32),
-                   dv.DevArray((N, 4, q), torch.int32), dv.DevArray((N, 6, q), torch.int64)]
+            res = [[dv.DevArray((q, N, k), torch.int32), dv.DevArray((q, N, k), torch.float32),
+                    dv.DevArray((N, 4, q), torch.int32), dv.DevArray((N, 6, q), torch.int64)]
+                   for _ in range(depth)]
+            flags = dv.DevArray((N + 1, depth), torch.int64)  # rows 0..N-1 landed[g], row N done
         handles = [None] * world
-        mine = {"inbox": self.inbox.ipc_handle(),
-                "res": [a.ipc_handle() for a in res] if res else None, "n": int(shard.n)}
+        mine = {"inbox": self.inbox.ipc_handle(), "n": int(shard.n),
+                "res": [[a.ipc_handle() for a in slot] for slot in res] if res else None,
+                "flags": flags.ipc_handle() if flags else None}
         dist.all_gather_object(handles, mine)
         nxt = (rank + 1) % world
         if world > 1:
             validate_inter(shard, handles[nxt]["n"])
-        self.next_inbox = self.inbox if nxt == rank else dv.DevArray((q,), torch.int64, handles[nxt]["inbox"])
+        self.next_inbox = self.inbox if nxt == rank else dv.DevArray((depth, q), torch.int64, handles[nxt]["inbox"])
         if rank == 0:
-            self.res = res
+            self.res, self.flags = res, flags
         else:
             shapes = [((q, N, k), torch.int32), ((q, N, k), torch.float32), ((N, 4, q), torch.int32),
                       ((N, 6, q), torch.int64)]
-            self.res = [dv.DevArray(sh, dt, h) for (sh, dt), h in zip(shapes, handles[0]["res"])]
-        self.final_ids = torch.empty((q, k), dtype=torch.int32, device=self.dev)
-        self.final_dists = torch.empty((q, k), dtype=torch.float32, device=self.dev)
-        self.err = dv.reduce_flag()
+            self.res = [[dv.DevArray(sh, dt, h) for (sh, dt), h in zip(shapes, slot)] for slot in handles[0]["res"]]
+            self.flags = dv.DevArray((N + 1, depth), torch.int64, handles[0]["flags"])
+        fp = self.flags.ptr
+        row = depth * 8  # bytes per flags row
 
-    def run(self, queries, params, mode: str, timer: list | None = None):
-        """Search all queries (every rank passes the full (Q, d) device batch);
-        returns final ids (Q, k) numpy on rank 0, None elsewhere."""
+        def ptrs(lst):
+            return torch.tensor(lst, dtype=torch.int64, device=self.dev)
+
+        # device arrays of flag pointers for pw_wait, per slot
+        self.landed_ptr = [fp + g * row + b * 8 for g in range(N) for b in range(depth)]
+        self.landed_all = [ptrs([fp + g * row + b * 8 for g in range(N)]) for b in range(depth)]
+        self.done_one = [ptrs([fp + N * row + b * 8]) for b in range(depth)]
+        self.final_ids = [torch.empty((q, k), dtype=torch.int32, device=self.dev) for _ in range(depth)]
+        self.final_dists = [torch.empty((q, k), dtype=torch.float32, device=self.dev) for _ in range(depth)]
+        self.err = dv.reduce_flag()
+        self.wait_err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.ready = [torch.cuda.Event() for _ in range(depth)]
+        self.last = 0
+        if rank == 0:
+            for b in range(depth):
+                self._reset(b)
+        torch.cuda.synchronize(self.dev)
+        dist.barrier()  # buffers clean on rank 0 before any peer writes
+
+    def _reset(self, b: int) -> None:
+        ids, dists, s32, s64 = self.res[b]
+        ids.t.fill_(-1)
+        dists.t.fill_(float("inf"))
+        s32.t.zero_()
+        s64.t.zero_()
+
+    def submit(self, queries, params, mode: str, timer: list | None = None) -> int:
+        """Enqueue one batch (every rank passes the full (Q, d) device batch);
+        returns its epoch.  No host synchronisation."""
         import ctypes as C
 
         import torch
-        import torch.distributed as dist
 
         from . import _abi
         from . import device as dv
 
-        g, N = self.rank, self.world
-        ids, dists, s32, s64 = self.res
+        lib = _abi.load()
+        g, N, depth = self.rank, self.world, self.depth
         self.epoch += 1
-        if g == 0:
-            ids.t.fill_(-1)
-            dists.t.fill_(float("inf"))
-            s32.t.zero_()
-            s64.t.zero_()
-        torch.cuda.synchronize(self.dev)
-        dist.barrier()  # rank 0's result buffers are clean and free
+        e = self.epoch
+        b = e % depth
+        ids, dists, s32, s64 = self.res[b]
+        st = self.stream.cuda_stream
+        if e > depth:  # the slot's previous batch (e - depth) must be reduced and its buffers reset
+            if g == 0:
+                self._reset(b)
+                _abi.check(lib.pw_signal(self.flags.ptr + N * depth * 8 + b * 8, e - depth, st))
+            else:
+                _abi.check(lib.pw_wait(self.done_one[b].data_ptr(), 1, e - depth, self.wait_err.data_ptr(), st))
         e0 = e1 = None
         if timer is not None:
             e0 = torch.cuda.Event(enable_timing=True)
@@ -322,40 +368,75 @@ class DataflowRing:
             e0.record(self.stream)
         if mode == "baseline" or N == 1:
             # pipeline.py:288-297: every rank searches every query at stage g
-            lib = _abi.load()
             p = _abi.params_struct(params)
             t = _abi.tuning_struct(self.tuning)
             _abi.check(lib.pw_search_stage(self.shard.handle, C.byref(p), C.byref(t), queries.data_ptr(),
                                            0, self.q, g, None, None, ids.ptr, dists.ptr, N, g,
                                            s32.ptr + g * 4 * self.q * 4, s64.ptr + g * 6 * self.q * 8,
-                                           self.q, self.stream.cuda_stream))
+                                           self.q, st))
         else:
-            dv.search_dataflow(self.shard, params, queries, g, N, self.epoch, self.inbox.ptr,
-                               self.next_inbox.ptr, ids.ptr, dists.ptr, s32.ptr, s64.ptr,
+            dv.search_dataflow(self.shard, params, queries, g, N, e, self.inbox.ptr + b * self.q * 8,
+                               self.next_inbox.ptr + b * self.q * 8, ids.ptr, dists.ptr, s32.ptr, s64.ptr,
                                tuning=self.tuning, sm_limit=self.sm_limit, stream=self.stream)
         if timer is not None:
             e1.record(self.stream)
             timer.append((e0, e1))
-        torch.cuda.synchronize(self.dev)
+        _abi.check(lib.pw_signal(self.landed_ptr[g * depth + b], e, st))
+        if g == 0:
+            _abi.check(lib.pw_wait(self.landed_all[b].data_ptr(), N, e, self.wait_err.data_ptr(), st))
+            _abi.check(lib.pw_reduce_topk(ids.ptr, dists.ptr, self.q, N * self.k, self.k,
+                                          self.final_ids[b].data_ptr(), self.final_dists[b].data_ptr(),
+                                          self.err.data_ptr(), st))
+        self.ready[b].record(self.stream)
+        self.last = e
+        return e
+
+    def _slot(self, e: int) -> int:
+        if not (self.last - self.depth < e <= self.last):
+            raise ValueError(f"batch {e} is no longer buffered (last {self.last}, depth {self.depth})")
+        return e % self.depth
+
+    def sync(self, e: int | None = None) -> None:
+        """Wait for batch e (default: the last) on this rank and raise on any
+        device-side error (a timed-out wait, a table overflow)."""
+        from . import device as dv
+
+        b = self._slot(self.last if e is None else e)
+        self.ready[b].synchronize()
+        if int(self.wait_err.item()):
+            self.wait_err.zero_()
+            raise RuntimeError("dataflow ring: a peer never signalled (pw_wait timed out)")
         dv.check_shard(self.shard)
-        dist.barrier()  # every column and counter has landed in rank 0's buffers
-        if g != 0:
+
+    def result(self, e: int | None = None):
+        """Final ids (Q, k) numpy of batch e (default: the last) on rank 0,
+        None elsewhere."""
+        from . import device as dv
+
+        e = self.last if e is None else e
+        self.sync(e)
+        if self.rank != 0:
             return None
-        lib = _abi.load()
-        _abi.check(lib.pw_reduce_topk(ids.ptr, dists.ptr, self.q, N * self.k, self.k,
-                                      self.final_ids.data_ptr(), self.final_dists.data_ptr(),
-                                      self.err.data_ptr(), self.stream.cuda_stream))
-        ids = self.final_ids.cpu().numpy()
+        ids = self.final_ids[self._slot(e)].cpu().numpy()
         dv.check_reduce_flag(self.err, self.dev)
         return ids
+
+    def run(self, queries, params, mode: str, timer: list | None = None):
+        """One batch, synchronously: final ids (Q, k) numpy on rank 0."""
+        return self.result(self.submit(queries, params, mode, timer=timer))
+
+    def last_final_dists(self):
+        return self.final_dists[self.last % self.depth]
 
     def last_stats(self) -> list[dict]:
         from .device import STAT_I32, STAT_I64
 
         if self.rank != 0:
             return []
-        s32 = self.res[2].t.cpu().numpy()
-        s64 = self.res[3].t.cpu().numpy()
+        self.sync()
+        slot = self.res[self.last % self.depth]
+        s32 = slot[2].t.cpu().numpy()
+        s64 = slot[3].t.cpu().numpy()
         out = []
         for s in range(self.world):
             st = {name: s32[s, i] for i, name in enumerate(STAT_I32)}
@@ -371,7 +452,7 @@ class DataflowRing:
         ids = self.run(qd, params, "pipelined")
         out = {"final_ids": ids}
         if self.rank == 0:
-            out["final_dists"] = self.final_dists.cpu().numpy()
+            out["final_dists"] = self.last_final_dists().cpu().numpy()
             out["bytes_out"] = out["final_ids"].nbytes + out["final_dists"].nbytes
         else:
             out["bytes_out"] = 0

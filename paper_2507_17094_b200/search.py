@@ -177,8 +177,6 @@ class DeviceShard:
         if ghost is not None:
             gids = np.ascontiguousarray(ghost.parent_ids, np.int32)
             gadj = np.ascontiguousarray(ghost.adj, np.int32)
-            if not np.array_equal(np.asarray(ghost.vectors, np.float32), vec[gids]):
-                raise ValueError("ghost vectors must be the parent shard's rows at parent_ids")
         if vec.shape[0] == 0:
             raise ValueError("empty graph")
         desc = _abi.ShardDesc(
@@ -188,7 +186,10 @@ class DeviceShard:
             0 if gids is None else gids.shape[0], 0 if gadj is None else gadj.shape[1],
             None if gids is None else gids.ctypes.data, None if gadj is None else gadj.ctypes.data, 0)
         h = C.c_void_p()
-        _abi.check(lib.pw_shard_create(C.byref(desc), C.byref(h)))
+        _abi.check(lib.pw_shard_create(C.byref(desc), C.byref(h)))  # validates every id range
+        if ghost is not None and not np.array_equal(np.asarray(ghost.vectors, np.float32), vec[gids]):
+            lib.pw_shard_destroy(h)
+            raise ValueError("ghost vectors must be the parent shard's rows at parent_ids")
         self.handle = h
         self.n = vec.shape[0]
         self.d = vec.shape[1]

@@ -267,10 +267,11 @@ LOSSY = {"flags": 2}
 
 
 @pytest.mark.parametrize("case", small_cases(), ids=lambda c: c[0])
-@pytest.mark.parametrize("slots", [8192, 64])
+@pytest.mark.parametrize("slots", [8192, 256])
 def test_small_golden_lossy_visited(small, case, slots):
     """Lossy visited cache: ids, distances and every counter but
-    distance_computations identical to the reference; 64 slots forces heavy
+    distance_computations identical to the reference; 256 slots (the
+    minimum) forces heavy
     forgetting, so re-scored queued nodes must be dropped by the merge."""
     name, params, mode, prefix = case
     if params.log_visits:
@@ -285,7 +286,7 @@ def test_small_golden_lossy_visited(small, case, slots):
 @pytest.mark.parametrize("d", [96, 128, 200, 960])
 @pytest.mark.parametrize("arm", range(len(SYNTH_ARMS)))
 @pytest.mark.parametrize("mode", ["baseline", "pipelined"])
-@pytest.mark.parametrize("slots", [8192, 128])
+@pytest.mark.parametrize("slots", [8192, 256])
 def test_synthetic_lossy_visited_matches_oracle(synth, d, arm, mode, slots):
     queries, ctxs = synth[d]
     params = SearchParams(**SYNTH_ARMS[arm])
@@ -294,3 +295,30 @@ def test_synthetic_lossy_visited_matches_oracle(synth, d, arm, mode, slots):
                              tuning=dict(LOSSY, visited_slots=slots)))
     want = oracle_dict(oracle.run(queries, ctxs, params, mode))
     assert_run_equal_lossy(got, want, f"d={d} arm={arm} {mode} lossy {slots}")
+
+
+def test_lossy_visited_ids_beyond_24_bits():
+    """The lossy cache's words hold epoch8 << 24 | the low bits of a bijective
+    hash, so shards of >= 2^24 nodes keep exact hits (a false hit would skip
+    a node and change the result).  17M points on a line (d = 1) with a
+    small-world graph; queries sit beyond id 2^24."""
+    import torch
+    n = (1 << 24) + 600_000
+    rs = np.random.default_rng(24)
+    x = np.arange(n, dtype=np.float32)[:, None] * np.float32(1.0 / 64)
+    off = np.array([-3, -2, -1, 1, 2, 3], np.int64)
+    idx = np.arange(n, dtype=np.int64)[:, None]
+    adj = np.empty((n, 8), np.int32)
+    adj[:, :6] = np.clip(idx + off, 0, n - 1)
+    adj[:, 6:] = rs.integers(0, n, (n, 2))  # long-range links
+    ctx = ShardContext(vectors=x, adj=adj, global_ids=np.arange(n, dtype=np.int32))
+    q = (np.float32((1 << 24) + 1000) + rs.random((64, 1), dtype=np.float32) * 500_000) / np.float32(64)
+    params = SearchParams(k=10, l=48, m=48, r=4, max_iter=48, seed=7)
+    want = oracle_dict(oracle.run(q, [ctx], params, "baseline"))
+    assert (want["final_ids"] >= (1 << 24)).mean() > 0.5
+    for slots in (4096, 256):
+        got = result_dict(pw.run_sharded_baseline(pw.Dataset(q), None, None, params, contexts=[ctx],
+                                                  tuning=dict(LOSSY, visited_slots=slots)))
+        assert_run_equal_lossy(got, want, f"ids >= 2^24 lossy {slots}")
+    del ctx
+    torch.cuda.empty_cache()
