@@ -414,12 +414,28 @@ def run_ours(args, cfg):
     pw_params = arm_params("pathweaver", ops["pathweaver"]["l"], k, metric, ops["pathweaver"]["discard"],
                            ops["pathweaver"]["ghost_iter"])
     search(pw_params, "pipelined")
-    dc_gathered = float(sum(s["distance_computations"].sum() for s in eng.last_stats())) / nq
+    lossy_stats = eng.last_stats()
+    dc_gathered = float(sum(s["distance_computations"].sum() for s in lossy_stats)) / nq
+    lossy_lists = engine_lists(eng) if rank == 0 else None
     exact_tuning = dict(tuning or {})
     exact_tuning["flags"] = int(exact_tuning.get("flags", 0)) & ~2
     eng_exact = engine(exact_tuning)
     eng_exact.run(queries, pw_params, "pipelined")
     stats = eng_exact.last_stats()
+    # ---- ID-level parity with the CPU oracle on the whole batch at this
+    # operating point (N=1: the oracle holds the same single shard)
+    parity = None
+    if rank == 0 and world == 1 and not args.no_parity:
+        import oracle
+
+        t0 = time.perf_counter()
+        ctx_host = host_index(W)
+        ref = oracle.run(W["queries"].cpu().numpy(), [ctx_host], pw_params, "pipelined",
+                         threads=os.cpu_count() or 1)
+        parity = parity_report({"exact_visited_run": engine_lists(eng_exact) + (stats,),
+                                "timed_lossy_run": lossy_lists + (lossy_stats,)}, ref, truth, k)
+        parity["oracle_s"] = round(time.perf_counter() - t0, 2)
+        del ctx_host
     seeded = set(range(1, world)) if world > 1 else set()
     bytes_step = dv.algorithmic_bytes(stats, pw_params, cfg["d"], cfg["j"], cfg["j_g"],
                                       esize=1 if cfg.get("dtype") == "u8" else 4,
@@ -521,6 +537,7 @@ def run_ours(args, cfg):
                               "sweep": ops["naive"]["sweep"],
                               "speedup_pathweaver_over_naive": round(qps / naive_qps, 3)},
             "cpu_baseline": cpu,
+            "parity": parity,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -564,6 +581,51 @@ def traffic_for(cfg: dict, l: int, discard: float = 0.5, ghost_iter: int = 8):
                                                        int(t.get("refine", 0)) == int(cfg.get("refine", 0)))):
                 return int(t["traffic_bytes_per_launch"])
     return None
+
+
+def engine_lists(eng):
+    """(final ids, final dists) numpy of the engine's last batch (rank 0)."""
+    if hasattr(eng, "run_buf"):
+        return eng.run_buf.final_ids.cpu().numpy(), eng.run_buf.final_dists.cpu().numpy()
+    ids = eng.result()
+    return ids, eng.last_final_dists().cpu().numpy()
+
+
+PARITY_COUNTERS = ("iterations", "ghost_iterations", "retained", "converged", "distance_computations",
+                   "total_visits", "inserted", "dgs_skipped")
+
+
+def parity_report(runs: dict, ref: dict, truth, k: int) -> dict:
+    """ID-level agreement of GPU runs with the CPU oracle on every query of the
+    bench batch at the chosen operating point (north_star: ids identical
+    except ties within 1e-5 relative, recall@k within 0.1 pt).  `runs` maps a
+    name to (final_ids, final_dists, stats); the lossy-visited run's
+    distance_computations legitimately differ, every other
+    counter must be equal."""
+    from paper_2507_17094_b200 import builder
+
+    rid, rd = ref["final_ids"], ref["final_dists"]
+    rrec = builder.recall_at_k(rid, truth, RECALL_AT)
+    out = {"queries": int(rid.shape[0]), "oracle": "oracle/pw_oracle.c (all host threads)",
+           "oracle_recall_at_10": round(rrec, 4)}
+    for name, (ids, dists, stats) in runs.items():
+        same_row = (ids == rid).all(axis=1)
+        # a differing id is acceptable only inside a distance tie (1e-5 rel)
+        tie_ok = np.isclose(dists, rd, rtol=1e-5, atol=0).all(axis=1)
+        counters = {}
+        for c in PARITY_COUNTERS:
+            g = np.stack([np.asarray(s[c]).astype(np.int64) for s in stats])
+            o = np.stack([np.asarray(s[c]).astype(np.int64) for s in ref["stages"]])
+            counters[c] = bool(np.array_equal(g, o))
+        out[name] = {
+            "ids_equal_frac": round(float(same_row.mean()), 6),
+            "ids_equal_or_tied_frac": round(float((same_row | tie_ok).mean()), 6),
+            "dists_bitequal_frac": round(float((dists.view(np.uint32) == rd.view(np.uint32)).all(axis=1)
+                                               .mean()), 6),
+            "counters_equal": counters,
+            "recall_delta": round(builder.recall_at_k(ids, truth, RECALL_AT) - rrec, 6),
+        }
+    return out
 
 
 def host_index(W: dict):
@@ -649,9 +711,15 @@ def run_reference(args, cfg):
         ok = chosen is not None
         chosen = chosen or sweep[-1][0]
         p = arm_params("pathweaver", chosen, k, metric, dr, gi)
-        t0 = time.perf_counter()
-        oracle.run(qh[:n], [ctx], p, "pipelined", threads=threads)
-        cands.append(dict(discard=dr, ghost_iter=gi, l=chosen, sweep=sweep, ok=ok, s=time.perf_counter() - t0))
+        # best of two timings per candidate (single samples are noisy on a
+        # shared host); every candidate's QPS is reported, so the GPU arm's
+        # operating point can be read off this line too
+        s = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            oracle.run(qh[:n], [ctx], p, "pipelined", threads=threads)
+            s.append(time.perf_counter() - t0)
+        cands.append(dict(discard=dr, ghost_iter=gi, l=chosen, sweep=sweep, ok=ok, s=min(s)))
     pool = [c for c in cands if c["ok"]] or cands
     best = min(pool, key=lambda c: c["s"])
     chosen, sweep = best["l"], best["sweep"]
@@ -670,9 +738,9 @@ def run_reference(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": cfg.get("dtype", "f32"), "data": "synthetic",
         "config": {"workload": cfg["workload"], "l": chosen, "sweep": sweep, "shards": 1,
                    "metric": metric, "dgs_discard": best["discard"], "ghost_max_iter": best["ghost_iter"],
-                   "pw_grid": {"columns": ["discard", "ghost_max_iter", "l", "recall", "sample_s"],
+                   "pw_grid": {"columns": ["discard", "ghost_max_iter", "l", "recall", "sample_s", "qps"],
                                "rows": [(c["discard"], c["ghost_iter"], c["l"], c["sweep"][-1][1],
-                                         round(c["s"], 3)) for c in cands]}},
+                                         round(c["s"], 3), round(n / c["s"], 1)) for c in cands]}},
         "cpu_baseline": {"value": round(qps, 1), "unit": "queries/s", "cores": threads,
                          "kind": "port",
                          "sample": f"{n} of {qh.shape[0]} queries per step (oracle/pw_oracle.c,"
@@ -692,6 +760,7 @@ def main():
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c2")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the whole-batch oracle comparison")
     ap.add_argument("--tuning", default=os.environ.get("PW_TUNING", DEFAULT_TUNING),
                     help='JSON device knobs, e.g. {"stage_rows": 16, "row_copy": 1}')
     args = ap.parse_args()

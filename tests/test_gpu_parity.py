@@ -322,3 +322,19 @@ def test_lossy_visited_ids_beyond_24_bits():
         assert_run_equal_lossy(got, want, f"ids >= 2^24 lossy {slots}")
     del ctx
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("mode", ["baseline", "pipelined"])
+@pytest.mark.parametrize("m,seed_mode", [(300, "neighbors"), (300, "mixed"), (1000, "mixed")])
+def test_initial_batch_choice_tail_shuffle(synth, mode, m, seed_mode):
+    """numpy Generator.choice(pop, m, replace=False) takes its tail-shuffle
+    branch when pop > 10000 and m > pop / 50 (the oracle is pinned to that
+    branch in rng.npz): 12000-node shards with m = 300 / 1000 random seeds
+    (search.py:222), with and without forwarded entries ahead of them."""
+    queries, ctxs = synth[96]
+    assert all(c.vectors.shape[0] > 10000 and m > c.vectors.shape[0] // 50 for c in ctxs)
+    params = SearchParams(k=10, l=64, m=m, r=8, max_iter=12, seed=11, seed_mode=seed_mode)
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(pw.Dataset(queries[:200]), None, None, params, contexts=ctxs))
+    want = oracle_dict(oracle.run(queries[:200], ctxs, params, mode))
+    assert_run_equal(got, want, f"choice tail m={m} {seed_mode} {mode}")
