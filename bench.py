@@ -44,6 +44,15 @@ CONFIGS = {
     "c2": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph",
                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
                spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
+    # C2 on harder data: intrinsic dimension 64 instead of 16 (same shape)
+    "c2h": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (latent dim 64)",
+                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=64, n_clusters=1,
+                spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
+    # C2 on the reference's own generator family (gen_synthetic: uniform
+    # centres + spread * N(0, I)), 10M rows in 100K clusters
+    "c2g": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (gen_synthetic family)",
+                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="gauss", n_clusters=100_000,
+                spread=0.08, rho=0.01, j_g=16, probe=192, refine=1),
     "c1": dict(workload="SIFT-shaped 100K x 128 f32, 1K queries, k=10, degree-32 graph",
                n=100_000, d=128, nq=1_000, k=10, j=32, gen="gauss", n_clusters=8192,
                spread=0.08, rho=0.01, j_g=16, probe=32, builder="exact"),

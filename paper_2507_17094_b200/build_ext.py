@@ -59,6 +59,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     counters, tools/phase_timers.py); the product library never has them."""
     out = PKG / "libpwb200_timers.so" if timers else OUT
     bdir = PKG / "_build_timers" if timers else BUILD
+    if os.environ.get("PW_LIB_OUT"):  # A/B variant builds (tools/ab.py --libs)
+        out = Path(os.environ["PW_LIB_OUT"]).resolve()
+        bdir = out.parent / ("_build_" + out.stem)
     if not force and (out.exists() and all(p.stat().st_mtime <= out.stat().st_mtime for p in DEPS)):
         return out
     bdir.mkdir(exist_ok=True)
@@ -89,7 +92,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     objs = [str(o) for _, o in jobs_list]
     _run([nv, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", str(out) + ".tmp", *objs])
     os.replace(str(out) + ".tmp", out)
-    if not timers:
+    if not timers and out == OUT:
         (PKG / "build_ptxas.log").write_text("\n".join(logs))
     if verbose:
         print("\n".join(logs))

@@ -156,8 +156,14 @@ def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: st
               tuning=None, stream=None, timer: list | None = None) -> None:
     """All shards on this device: baseline (shard s = stage s, all queries) or
     pipelined (chunk c stage s on shard (c+s)%N, entry forwarded in HBM).
-    If `timer` is a list, (start, end) CUDA events bracket every search launch."""
+    If `timer` is a list, (start, end) CUDA events bracket every search launch.
+    `params` may be a list of N SearchParams, one per stage (per-stage
+    budgets, SPEC.md "a per-stage budget vector is configurable"; an opt-in
+    extension -- the reference's run_pipelined uses one parameter set)."""
     n = len(shards)
+    per_stage = list(params) if isinstance(params, (list, tuple)) else [params] * n
+    if len(per_stage) != n or len({p.k for p in per_stage}) != 1:
+        raise ValueError("per-stage params: one SearchParams per stage, all with the same k")
     q = queries.shape[0]
     stream = stream or torch.cuda.current_stream(queries.device)
 
@@ -175,14 +181,14 @@ def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: st
         run.reset()
     if mode == "baseline":
         for s in range(n):
-            launch(shards[s], params, queries, 0, q, s, run, s, s)
+            launch(shards[s], per_stage[s], queries, 0, q, s, run, s, s)
     else:
         lo = chunk_bounds(q, n)
         ein, eout = run.entries
         for stage in range(n):
             for c in range(n):
                 shard = (c + stage) % n
-                launch(shards[shard], params, queries, lo[c], lo[c + 1] - lo[c], stage, run, shard,
+                launch(shards[shard], per_stage[stage], queries, lo[c], lo[c + 1] - lo[c], stage, run, shard,
                        stage, entries_in=ein if stage > 0 else None,
                        forward_out=eout if stage < n - 1 else None)
             ein, eout = eout, ein
