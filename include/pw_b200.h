@@ -64,6 +64,15 @@ typedef struct {
                                 bit 1: lossy visited cache (ids exact, distance_computations may grow);
                                 bit 2: TMA bulk copies for expansion rows (bits 0 and 2 are measured slower;
                                 kept for A/B) */
+    /* Opt-in path-extension knobs beyond the reference (its run_pipelined
+     * forwards exactly one entry per query and uses one budget for every
+     * stage; SPEC.md "DESIGN DECISIONS" names both as configurable).  0 =
+     * the reference's behaviour; results then differ from the reference. */
+    int32_t forward_count;   /* entries forwarded per query to the next shard (top-F of the
+                                stage's queue through inter_map); 1..8.  Entry
+                                buffers / inboxes then hold F words per query. */
+    int32_t late_l;          /* queue length l of stages >= 1 (k <= late_l); 0 = params->l */
+    int32_t late_max_iter;   /* max_iter of stages >= 1; 0 = params->max_iter */
 } pw_tuning;
 
 /* One shard (pipeline.py:121-155 build_contexts output for one ShardPack):

@@ -53,7 +53,8 @@ class _Params(C.Structure):
         ("discard_ratio", C.c_double), ("cooldown_ratio", C.c_double),
         ("ghost_enabled", C.c_int32), ("ghost_max_iter", C.c_int32),
         ("seed_mode", C.c_int32), ("buffer_cap", C.c_int32), ("log_visits", C.c_int32),
-        ("metric", C.c_int32),
+        ("metric", C.c_int32), ("forward_count", C.c_int32), ("late_l", C.c_int32),
+        ("late_max_iter", C.c_int32),
     ]
 
 
@@ -190,12 +191,16 @@ def in_cooldown(iteration: int, max_iter: int, cooldown_ratio: float) -> bool:
 
 
 # --------------------------------------------------------------- search
-def _params(p) -> _Params:
+def _params(p, ext: dict | None = None) -> _Params:
+    """ext: the opt-in path-extension knobs (forward_count, late_l,
+    late_max_iter; the GPU's tuning keys of the same names)."""
+    ext = ext or {}
     return _Params(int(p.k), int(p.l), int(p.m), int(p.r), int(p.max_iter),
                    int(p.seed) & (2**64 - 1), SELECTION[p.selection], float(p.discard_ratio),
                    float(p.cooldown_ratio), int(bool(p.ghost_enabled)), int(p.ghost_max_iter),
                    SEED_MODE[p.seed_mode], int(p.buffer_cap or 0), int(bool(p.log_visits)),
-                   {"l2": 0, "ip": 1}[getattr(p, "metric", "l2")])
+                   {"l2": 0, "ip": 1}[getattr(p, "metric", "l2")], int(ext.get("forward_count", 0)),
+                   int(ext.get("late_l", 0)), int(ext.get("late_max_iter", 0)))
 
 
 class _Keep:
@@ -282,15 +287,16 @@ STAT_I32 = ("iterations", "ghost_iterations", "retained", "converged")
 STAT_I64 = ("distance_computations", "total_visits", "inserted", "dgs_skipped")
 
 
-def run(queries: np.ndarray, contexts, params, mode: str, threads: int = 0) -> dict:
-    """pipeline.py run_sharded_baseline (mode='baseline') / run_pipelined."""
+def run(queries: np.ndarray, contexts, params, mode: str, threads: int = 0, ext: dict | None = None) -> dict:
+    """pipeline.py run_sharded_baseline (mode='baseline') / run_pipelined.
+    ext: opt-in path-extension knobs (not the reference; see _params)."""
     keep = _Keep()
     n = len(contexts)
     arr = (_Shard * n)(*[_shard(keep, c) for c in contexts])
     q = keep.arr(queries, np.float32)
     nq = q.shape[0]
     k = int(params.k)
-    p = _params(params)
+    p = _params(params, ext)
     shard_ids = np.empty((nq, n, k), np.int32)
     shard_dists = np.empty((nq, n, k), np.float32)
     final_ids = np.empty((nq, k), np.int32)

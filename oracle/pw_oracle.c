@@ -641,18 +641,31 @@ typedef struct {
 #define TAG_SEARCH 4
 #define TAG_GHOST_SEARCH 5
 
+/* stage >= 1 parameters (opt-in late budgets; the reference uses p itself) */
+static orc_params stage_params(const orc_params* p, int32_t stage) {
+    orc_params q = *p;
+    if (stage > 0 && p->late_l > 0) q.l = p->late_l;
+    if (stage > 0 && p->late_max_iter > 0) q.max_iter = p->late_max_iter;
+    return q;
+}
+
+static int32_t fwd_count(const orc_params* p) { return p->forward_count > 0 ? p->forward_count : 1; }
+
 static int search_one(run_t* R, int64_t qid, int32_t shard, int32_t stage, int has_seed,
-                      int64_t entry_in, int32_t* top_local) {
-    const orc_params* p = R->p;
+                      const int64_t* entry_in, int32_t* top_local) {
+    const orc_params ps = stage_params(R->p, stage);
+    const orc_params* p = &ps;
+    const int32_t F = fwd_count(R->p);
     const orc_shard* sh = &R->shards[shard];
     const float* query = R->queries + qid * R->d;
     const int64_t Q = R->q;
     int32_t* it32 = R->s32 + (int64_t)stage * 4 * Q;
     int64_t* it64 = R->s64 + (int64_t)stage * 4 * Q;
-    int64_t seeds_buf[1 + 4096];
+    int64_t seeds_buf[8 * (1 + 512)];
     int64_t* seeds = seeds_buf;
     int32_t n_seeds = 0;
-    if (has_seed) seeds[n_seeds++] = entry_in;
+    if (has_seed)
+        for (int32_t f = 0; f < F; f++) seeds[n_seeds++] = entry_in[f];
     if (p->ghost_enabled && !has_seed && sh->has_ghost) {
         uint64_t parts[3] = {TAG_GHOST_SEARCH, (uint64_t)qid, (uint64_t)stage};
         orc_pcg64 g;
@@ -666,12 +679,16 @@ static int search_one(run_t* R, int64_t qid, int32_t shard, int32_t stage, int h
         it64[1 * Q + qid] += gc.total_visits;
     }
     if (n_seeds && p->seed_mode == 0) {
+        /* [e] + adj[e] (pipeline.py:229-231); F entries: [e_0..e_F-1] + adj[e_0] + ... */
         int32_t j = sh->main.j;
-        int64_t e = seeds[0];
-        if (j + 1 > 4096) seeds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(j + 1));
-        seeds[0] = e;
-        for (int32_t t = 0; t < j; t++) seeds[1 + t] = sh->main.adj[e * j + t];
-        n_seeds = 1 + j;
+        int64_t e[8];
+        const int32_t ne = n_seeds;
+        for (int32_t f = 0; f < ne; f++) e[f] = seeds[f];
+        if ((int64_t)ne * (1 + j) > 8 * (1 + 512)) seeds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(ne * (1 + j)));
+        for (int32_t f = 0; f < ne; f++) seeds[f] = e[f];
+        for (int32_t f = 0; f < ne; f++)
+            for (int32_t t = 0; t < j; t++) seeds[ne + f * j + t] = sh->main.adj[e[f] * j + t];
+        n_seeds = ne * (1 + j);
     }
     uint64_t parts[3] = {TAG_SEARCH, (uint64_t)qid, (uint64_t)stage};
     orc_pcg64 g;
@@ -701,7 +718,8 @@ static int search_one(run_t* R, int64_t qid, int32_t shard, int32_t stage, int h
             R->shard_ids[base + t] = pid[t];
             R->shard_dists[base + t] = pd[t];
         }
-        *top_local = r.n_out ? ploc[0] : -1;
+        /* top-F local ids (short lists repeat their last entry) */
+        for (int32_t f = 0; f < F; f++) top_local[f] = r.n_out ? ploc[f < r.n_out ? f : r.n_out - 1] : -1;
     }
     if (pid != ids) { free(pid); free(ploc); free(pd); }
     return rc;
@@ -728,13 +746,18 @@ int orc_run_stage(const orc_shard* shard, const float* queries, int64_t q_total,
 #pragma omp parallel for schedule(dynamic, 4)
     for (int64_t qi = q0; qi < q0 + n; qi++) {
         if (err) continue;
-        int32_t tl = -1;
-        if (search_one(&R, qi, col, stage, entries_in != NULL, entries_in ? entries_in[qi] : 0, &tl)) {
+        const int32_t F = fwd_count(p);
+        int32_t tl[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+        int64_t ein[8] = {0};
+        if (entries_in)
+            for (int32_t f = 0; f < F; f++) ein[f] = entries_in[qi * F + f];
+        if (search_one(&R, qi, col, stage, entries_in != NULL, ein, tl)) {
 #pragma omp critical
             { err = 1; snprintf(errbuf, sizeof errbuf, "%s", g_err); }
             continue;
         }
-        if (forward_out) forward_out[qi] = shard->inter_map[tl];
+        if (forward_out)
+            for (int32_t f = 0; f < F; f++) forward_out[qi * F + f] = shard->inter_map[tl[f]];
     }
     free(arr);
     if (err) { snprintf(g_err, sizeof g_err, "%s", errbuf); return -1; }
@@ -767,8 +790,8 @@ int orc_run(const orc_shard* shards, int32_t n_shards, const float* queries, int
 #pragma omp parallel for schedule(dynamic, 4)
             for (int64_t qi = 0; qi < q; qi++) {
                 if (err) continue;
-                int32_t tl;
-                if (search_one(&R, qi, s, s, 0, 0, &tl)) {
+                int32_t tl[8];
+                if (search_one(&R, qi, s, s, 0, NULL, tl)) {
 #pragma omp critical
                     { err = 1; snprintf(errbuf, sizeof errbuf, "%s", g_err); }
                 }
@@ -780,7 +803,8 @@ int orc_run(const orc_shard* shards, int32_t n_shards, const float* queries, int
         int64_t base = q / N, extra = q % N;
         lo[0] = 0;
         for (int32_t c = 0; c < N; c++) lo[c + 1] = lo[c] + base + (c < extra ? 1 : 0);
-        int64_t* entries = (int64_t*)malloc(sizeof(int64_t) * (size_t)(q > 0 ? q : 1));
+        const int32_t F = fwd_count(p);
+        int64_t* entries = (int64_t*)malloc(sizeof(int64_t) * (size_t)(q > 0 ? q * F : 1));
         for (int32_t stage = 0; stage < N; stage++) {
             for (int32_t c = 0; c < N; c++) {
                 int32_t shard = (c + stage) % N;
@@ -788,15 +812,16 @@ int orc_run(const orc_shard* shards, int32_t n_shards, const float* queries, int
 #pragma omp parallel for schedule(dynamic, 4)
                 for (int64_t qi = lo[c]; qi < lo[c + 1]; qi++) {
                     if (err) continue;
-                    int32_t tl = -1;
-                    if (search_one(&R, qi, shard, stage, stage > 0, entries[qi], &tl)) {
+                    int32_t tl[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+                    if (search_one(&R, qi, shard, stage, stage > 0, entries + qi * F, tl)) {
 #pragma omp critical
                         { err = 1; snprintf(errbuf, sizeof errbuf, "%s", g_err); }
                         continue;
                     }
-                    if (forward) entries[qi] = shards[shard].inter_map[tl];
+                    if (forward)
+                        for (int32_t f = 0; f < F; f++) entries[qi * F + f] = shards[shard].inter_map[tl[f]];
                 }
-                if (forward) comm[(int64_t)stage * N + shard] = 4 * (lo[c + 1] - lo[c]);
+                if (forward) comm[(int64_t)stage * N + shard] = 4 * F * (lo[c + 1] - lo[c]);
             }
         }
         free(lo);

@@ -52,6 +52,11 @@ typedef struct {
     int32_t buffer_cap;       /* 0 = None */
     int32_t log_visits;
     int32_t metric;           /* 0 L2 (the reference); 1 inner product (extension, parity unpinned) */
+    /* opt-in path-extension knobs (the GPU's pw_tuning fields of the same
+     * names; 0 = the reference's run_pipelined) */
+    int32_t forward_count;    /* top-F entries forwarded per query (F <= k) */
+    int32_t late_l;           /* l of stages >= 1 */
+    int32_t late_max_iter;    /* max_iter of stages >= 1 */
 } orc_params;
 
 /* numpy PCG64 bit generator state (128-bit state/inc + buffered uint32). */

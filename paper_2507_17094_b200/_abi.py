@@ -31,7 +31,8 @@ class Params(C.Structure):
 
 class Tuning(C.Structure):
     _fields_ = [("visited_slots", C.c_int32), ("stage_rows", C.c_int32),
-                ("warps_per_sm", C.c_int32), ("row_copy", C.c_int32), ("flags", C.c_int32)]
+                ("warps_per_sm", C.c_int32), ("row_copy", C.c_int32), ("flags", C.c_int32),
+                ("forward_count", C.c_int32), ("late_l", C.c_int32), ("late_max_iter", C.c_int32)]
 
 
 class ShardDesc(C.Structure):
@@ -161,9 +162,15 @@ METRIC = {"l2": 0, "ip": 1}
 
 def tuning_struct(t) -> Tuning:
     if t is None:
-        return Tuning(0, 0, 0, 0, 0)
+        return Tuning(0, 0, 0, 0, 0, 0, 0, 0)
     return Tuning(int(t.get("visited_slots", 0)), int(t.get("stage_rows", 0)),
-                  int(t.get("warps_per_sm", 0)), int(t.get("row_copy", 0)), int(t.get("flags", 0)))
+                  int(t.get("warps_per_sm", 0)), int(t.get("row_copy", 0)), int(t.get("flags", 0)),
+                  int(t.get("forward_count", 0)), int(t.get("late_l", 0)), int(t.get("late_max_iter", 0)))
+
+
+def forward_count(t) -> int:
+    """Entries forwarded per query (tuning "forward_count", default 1)."""
+    return max(1, int((t or {}).get("forward_count", 0) or 1))
 
 
 def launch_config(shard_handle, params, tuning=None) -> dict:

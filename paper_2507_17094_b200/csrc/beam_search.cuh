@@ -73,6 +73,9 @@ struct KArgs {
     int32_t spad;           // staging row stride in elements (bank-conflict-free passes)
     L2Plan plan;
     SearchCfg cfg, gcfg;
+    SearchCfg cfg_late;     // stages >= 1 when has_late (opt-in per-stage budgets)
+    int32_t has_late;
+    int32_t fwd;            // entries forwarded per query (1 = the reference)
     int32_t ghost_on;       // run the ghost prologue when the task has no entry
     int32_t seed_mode;      // 0 neighbors, 1 mixed
     int32_t use_ghost_graph;
@@ -1728,7 +1731,12 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
         int64_t row = task;  // query / output / stats row
         int32_t stage = A.stage;
         bool has_entry = A.entries != nullptr;
-        int32_t entry = has_entry ? A.entries[task] : -1;
+        // forwarded entries land in cand[0..n_ent) (the seed list's head)
+        int n_ent = 0;
+        if (has_entry) {
+            if ((int)lane < A.fwd) S.cand[lane] = A.entries[(int64_t)task * A.fwd + lane];
+            n_ent = A.fwd;
+        }
         if (A.df) {
             // stage-major task list of shard g: stage s searches chunk (g - s) mod N
             stage = 0;
@@ -1738,23 +1746,29 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
             row = qid;
             has_entry = stage > 0;
             if (has_entry) {
-                unsigned long long v = 0;
                 if (lane == 0) {
                     // bounded wait (~10 s): a producer that never comes (a
                     // shard not resident, a dead peer) raises an error
-                    // instead of hanging the GPU
-                    for (uint32_t spin = 0;; spin++) {
-                        v = ld_acquire_sys(A.df_inbox + qid);
-                        if ((uint32_t)(v >> 32) == A.df_epoch) break;
-                        if (spin > (1u << 25)) {
-                            atomicOr(A.err, 16);
-                            v = 0;
-                            break;
+                    // instead of hanging the GPU.  F words per query, each
+                    // stored with release semantics: poll them in order.
+                    uint32_t spin = 0;
+                    for (int f = 0; f < A.fwd; f++) {
+                        unsigned long long v = 0;
+                        for (;; spin++) {
+                            v = ld_acquire_sys(A.df_inbox + qid * A.fwd + f);
+                            if ((uint32_t)(v >> 32) == A.df_epoch) break;
+                            if (spin > (1u << 25)) {
+                                atomicOr(A.err, 16);
+                                v = 0;
+                                break;
+                            }
+                            __nanosleep(256);
                         }
-                        __nanosleep(256);
+                        S.cand[f] = (int32_t)(uint32_t)v;
                     }
                 }
-                entry = (int32_t)(uint32_t)__shfl_sync(0xffffffffu, (unsigned)v, 0);
+                n_ent = A.fwd;
+                __syncwarp();
             }
         }
         // query row -> smem
@@ -1817,11 +1831,15 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
                     ns = A.n_seeds;
                     fill_random = A.seed_mode == 1;
                 } else if (has_entry) {
-                    if (lane == 0) S.cand[0] = entry;
-                    ns = 1;
+                    // [e] + adj[e] (pipeline.py:229-231); with F forwarded
+                    // entries (opt-in): [e_0..e_F-1] + adj[e_0] + ... + adj[e_F-1]
+                    ns = n_ent;
                     if (A.seed_mode == 0) {
-                        for (int t = lane; t < G.j; t += 32) S.cand[1 + t] = G.adj[(size_t)entry * G.j + t];
-                        ns = 1 + G.j;
+                        for (int f = 0; f < n_ent; f++) {
+                            const int32_t e = S.cand[f];
+                            for (int t = lane; t < G.j; t += 32) S.cand[n_ent + f * G.j + t] = G.adj[(size_t)e * G.j + t];
+                        }
+                        ns = n_ent * (1 + G.j);
                         fill_random = false;
                     }
                 }
@@ -1829,10 +1847,13 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
                 rng = A.rng_io ? A.rng_io[task]
                                : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)tsk[0], (uint64_t)tsk[1]));
             }
-            converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G, gph ? A.gcfg : A.cfg, ns, fill_random,
-                                      rng, task, &n_logged);
+            converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G,
+                                             gph ? A.gcfg : (A.has_late && tsk[1] > 0 ? A.cfg_late : A.cfg),
+                                             ns, fill_random, rng, task, &n_logged);
             if (gph) {
-                entry = A.ghost.gid[(uint32_t)S.qk_cur()[0]];
+                if (lane == 0) S.cand[0] = A.ghost.gid[(uint32_t)S.qk_cur()[0]];
+                __syncwarp();
+                n_ent = 1;
                 has_entry = true;
                 g_it = (int32_t)S.c_it;
                 g_dc = S.c_dc;
@@ -1867,9 +1888,13 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
                 A.out_dists[row * A.out_stride + t] = __int_as_float(0x7f800000);
             }
             if (lane == 0) {
-                if (stage + 1 < A.df_N)  // pipeline.py:339 forward inter_map[top1] to shard g+1
-                    st_release_sys(A.df_next + qid, ((unsigned long long)A.df_epoch << 32) |
-                                                        (uint32_t)(nk > 0 ? A.inter[(uint32_t)qk[0]] : 0));
+                // pipeline.py:339 forward inter_map[top1] to shard g+1 (opt-in:
+                // the top F, short queues repeating their last entry)
+                if (stage + 1 < A.df_N)
+                    for (int f = 0; f < A.fwd; f++)
+                        st_release_sys(A.df_next + qid * A.fwd + f,
+                                       ((unsigned long long)A.df_epoch << 32) |
+                                           (uint32_t)(nk > 0 ? A.inter[(uint32_t)qk[min(f, S.qlen - 1)]] : 0));
                 if (A.st32) {
                     int32_t* s32 = A.st32 + stage * A.st32_stage_stride + qid;
                     int64_t* s64 = A.st64 + stage * A.st64_stage_stride + qid;
@@ -1885,8 +1910,11 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
                     s64[5 * A.st_stride] = g_ne;
                 }
             }
-        } else if (lane == 0) {
-            if (A.forward && nk > 0) A.forward[task] = A.inter[(uint32_t)qk[0]];
+        } else {
+            if (A.forward && nk > 0 && (int)lane < A.fwd)
+                A.forward[(int64_t)task * A.fwd + lane] = A.inter[(uint32_t)qk[min((int)lane, S.qlen - 1)]];
+        }
+        if (!A.df && lane == 0) {
             if (A.st32) {
                 A.st32[0 * A.st_stride + task] += (int32_t)S.c_it;
                 A.st32[1 * A.st_stride + task] += g_it;

@@ -497,6 +497,18 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     gp.log_visits = 0;
     gp.buffer_cap = 0;
     A.gcfg = make_cfg(gp, std::max<int64_t>(sh->gn, 1), sh->gj);
+    // opt-in path-extension knobs (pw_tuning: forward_count, late_l, late_max_iter)
+    A.fwd = (tun && tun->forward_count > 0) ? tun->forward_count : 1;
+    if (A.fwd > 8 || A.fwd > p.k) return set_err(PW_EINVAL, "forward_count must be in [1, min(8, k)]");
+    pw_params lp = p;
+    if (tun && tun->late_l > 0) lp.l = tun->late_l;
+    if (tun && tun->late_max_iter > 0) lp.max_iter = tun->late_max_iter;
+    A.has_late = (lp.l != p.l || lp.max_iter != p.max_iter) ? 1 : 0;
+    if (A.has_late) {
+        if ((rc = validate_params(lp))) return rc;
+        A.cfg_late = make_cfg(lp, G.n, G.j);
+    }
+    const int32_t Lq = std::max(p.l, lp.l);  // queue capacity (smem layout)
     A.ghost_on = ghost_on ? 1 : 0;
     A.seed_mode = p.seed_mode;
     A.use_ghost_graph = use_ghost_graph ? 1 : 0;
@@ -529,13 +541,14 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         while (!ok(spad)) spad += 16;
     }
     A.spad = spad;
-    int64_t cb = std::max<int64_t>({(int64_t)p.r * jm, (int64_t)A.cfg.want, (int64_t)1 + jm,
+    int64_t cb = std::max<int64_t>({(int64_t)p.r * jm, (int64_t)A.cfg.want, (int64_t)A.fwd * (1 + jm),
                                     (int64_t)n_seeds, (int64_t)A.gcfg.want, 32});
     cb = (cb + 31) / 32 * 32;
     A.CB = (int32_t)cb;
     A.BH = (int32_t)next_pow2(2 * cb);
-    A.L_max = p.l;
+    A.L_max = Lq;
     int64_t bound = visit_bound(A.cfg, G.j, G.n);
+    if (A.has_late) bound = std::max(bound, visit_bound(A.cfg_late, G.j, G.n));
     if (ghost_on) bound = std::max(bound, visit_bound(A.gcfg, sh->gj, sh->gn));
     // Default: a small shared-memory visited table (first iterations) backed
     // by the per-warp epoch-tagged global table (batched probes): measured on
@@ -608,8 +621,8 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         // (sum q^2, integral flag) for the exact integer distance path
         A.o_q = (int32_t)off;
         off = al(off + 4 * (int64_t)((d + 3) & ~3) + (elem == 1 ? ((d + 15) & ~15) + 16 : 0));
-        A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)p.l);  // one queue buffer (in-place merge)
-        A.o_qe = (int32_t)off; off = al(off + (int64_t)p.l);
+        A.o_qk = (int32_t)off; off = al(off + 8 * (int64_t)Lq);  // one queue buffer (in-place merge)
+        A.o_qe = (int32_t)off; off = al(off + (int64_t)Lq);
         A.o_newl = (int32_t)off; off = al(off + 4 * cb);
         // keys (pow2 for the survivor sort); the candidate list lives in their
         // upper half: candidates are live from expansion to the dedup, while the
@@ -892,8 +905,8 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
     A.q0 = q0;
     A.n_tasks = (int32_t)n;
     A.queries = queries + q0 * sh->d;
-    A.entries = entries_in ? entries_in + q0 : nullptr;
-    A.forward = forward_out ? forward_out + q0 : nullptr;
+    A.entries = entries_in ? entries_in + q0 * A.fwd : nullptr;
+    A.forward = forward_out ? forward_out + q0 * A.fwd : nullptr;
     const int64_t k = params->k;
     A.out_ids = shard_ids + (q0 * n_cols + col) * k;
     A.out_dists = shard_dists + (q0 * n_cols + col) * k;
@@ -1112,7 +1125,8 @@ int run_dataflow_local(RunWs& W, pw_shard* const* shards, int32_t N, const pw_pa
         if (!W.ev[g]) PW_CUDA(cudaEventCreateWithFlags(&W.ev[g], cudaEventDisableTiming));
     }
     if (!W.ev[8]) PW_CUDA(cudaEventCreateWithFlags(&W.ev[8], cudaEventDisableTiming));
-    const size_t words = (size_t)N * (size_t)q;
+    const int F = (tuning && tuning->forward_count > 0) ? tuning->forward_count : 1;
+    const size_t words = (size_t)N * (size_t)q * F;
     if (W.inbox_cap < words) {
         PW_CUDA(cudaStreamSynchronize(st));
         if (W.inbox) cudaFree(W.inbox);
@@ -1136,7 +1150,7 @@ int run_dataflow_local(RunWs& W, pw_shard* const* shards, int32_t N, const pw_pa
     for (int g = 0; g < N; g++) {
         PW_CUDA(cudaStreamWaitEvent(W.ring[g], W.ev[8], 0));
         rc = pw_search_dataflow(shards[g], params, tuning, queries, q, g, N, W.epoch,
-                                W.inbox + (size_t)g * q, W.inbox + (size_t)((g + 1) % N) * q, shard_ids,
+                                W.inbox + (size_t)g * q * F, W.inbox + (size_t)((g + 1) % N) * q * F, shard_ids,
                                 shard_dists, stats_i32, stats_i64, sm_limit, W.ring[g]);
         if (rc) return rc;
         PW_CUDA(cudaEventRecord(W.ev[g], W.ring[g]));
@@ -1230,6 +1244,7 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     if (!W.st) PW_CUDA(cudaStreamCreateWithFlags(&W.st, cudaStreamNonBlocking));
     cudaStream_t st = W.st;
     const int64_t qq = std::max<int64_t>(q, 1);
+    const int64_t F = (tuning && tuning->forward_count > 0) ? tuning->forward_count : 1;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         size_t o = off;
@@ -1239,8 +1254,8 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     size_t o_q = take(sizeof(float) * qq * d), o_sid = take(sizeof(int32_t) * qq * N * k),
            o_sd = take(sizeof(float) * qq * N * k), o_fid = take(sizeof(int32_t) * qq * k),
            o_fd = take(sizeof(float) * qq * k), o_s32 = take(sizeof(int32_t) * qq * N * 4),
-           o_s64 = take(sizeof(int64_t) * qq * N * 6), o_ea = take(sizeof(int32_t) * qq),
-           o_eb = take(sizeof(int32_t) * qq), o_err = take(sizeof(int32_t));
+           o_s64 = take(sizeof(int64_t) * qq * N * 6), o_ea = take(sizeof(int32_t) * qq * F),
+           o_eb = take(sizeof(int32_t) * qq * F), o_err = take(sizeof(int32_t));
     if ((rc = ws_reserve(W, off))) return rc;
     char* b = W.buf;
     float* dq = (float*)(b + o_q);
@@ -1268,13 +1283,13 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     for (int s = 0; s < N; s++)
         if ((rc = check_err(shards[s]))) return rc;
     if (herr) return set_err(PW_EINVAL, "cannot reduce empty candidate lists");
-    // comm accounting (pipeline.py:340-341): 4 B per forwarded query
+    // comm accounting (pipeline.py:340-341): 4 B per forwarded entry
     std::memset(comm, 0, sizeof(int64_t) * N * N);
     if (mode == PW_MODE_PIPELINED) {
         std::vector<int64_t> lo(N + 1, 0);
         for (int c = 0; c < N; c++) lo[c + 1] = lo[c] + q / N + (c < q % N ? 1 : 0);
         for (int stage = 0; stage < N - 1; stage++)
-            for (int c = 0; c < N; c++) comm[(int64_t)stage * N + (c + stage) % N] = 4 * (lo[c + 1] - lo[c]);
+            for (int c = 0; c < N; c++) comm[(int64_t)stage * N + (c + stage) % N] = 4 * F * (lo[c + 1] - lo[c]);
     }
     return 0;
 }

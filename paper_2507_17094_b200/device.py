@@ -93,7 +93,8 @@ class DeviceRun:
         self.final_dists = torch.empty((q, k), dtype=torch.float32, device=dev)
         self.s32 = torch.empty((n_cols, 4, q), dtype=torch.int32, device=dev)
         self.s64 = torch.empty((n_cols, 6, q), dtype=torch.int64, device=dev)
-        self.entries = [torch.zeros(q, dtype=torch.int32, device=dev) for _ in range(2)]
+        # forwarded entries, up to 8 per query (tuning "forward_count", opt-in)
+        self.entries = [torch.zeros(q * 8, dtype=torch.int32, device=dev) for _ in range(2)]
         self.err = reduce_flag()
 
     def reset(self):
@@ -252,7 +253,8 @@ class LocalDataflow:
         self.shards = shards
         self.n = len(shards)
         dev = torch.device(device)
-        self.inbox = [torch.zeros(q, dtype=torch.int64, device=dev) for _ in range(self.n)]
+        # up to 8 entry words per query (tuning "forward_count", opt-in)
+        self.inbox = [torch.zeros(q * 8, dtype=torch.int64, device=dev) for _ in range(self.n)]
         self.streams = [torch.cuda.Stream(dev) for _ in range(self.n)]
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         self.sm_limit = max(1, sms // self.n)

@@ -22,6 +22,12 @@ from __future__ import annotations
 import numpy as np
 
 
+def _abi_forward_count(tuning) -> int:
+    from ._abi import forward_count
+
+    return forward_count(tuning)
+
+
 def chunk_bounds(q: int, n: int) -> list[int]:
     """np.array_split(arange(q), n) boundaries (pipeline.py:327)."""
     lo = [0]
@@ -119,6 +125,8 @@ class RingSearch:
         from . import device as dv
 
         R = self.run_buf
+        if self.world > 1 and _abi_forward_count(self.tuning) > 1:
+            raise ValueError("forward_count > 1 needs the dataflow ring (PW_RING=dataflow)")
         if self.world == 1:
             dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning,
                          stream=self.stream, timer=timer)
@@ -286,7 +294,7 @@ class DataflowRing:
         self.depth = depth
         self.epoch = 0
         N = world
-        self.inbox = dv.DevArray((depth, q), torch.int64)
+        self.inbox = dv.DevArray((depth, q * 8), torch.int64)  # <= 8 entry words per query
         res = flags = None
         if rank == 0:
             res = [[dv.DevArray((q, N, k), torch.int32), dv.DevArray((q, N, k), torch.float32),
@@ -301,7 +309,7 @@ class DataflowRing:
         nxt = (rank + 1) % world
         if world > 1:
             validate_inter(shard, handles[nxt]["n"])
-        self.next_inbox = self.inbox if nxt == rank else dv.DevArray((depth, q), torch.int64, handles[nxt]["inbox"])
+        self.next_inbox = self.inbox if nxt == rank else dv.DevArray((depth, q * 8), torch.int64, handles[nxt]["inbox"])
         if rank == 0:
             self.res, self.flags = res, flags
         else:
@@ -375,8 +383,8 @@ class DataflowRing:
                                            s32.ptr + g * 4 * self.q * 4, s64.ptr + g * 6 * self.q * 8,
                                            self.q, st))
         else:
-            dv.search_dataflow(self.shard, params, queries, g, N, e, self.inbox.ptr + b * self.q * 8,
-                               self.next_inbox.ptr + b * self.q * 8, ids.ptr, dists.ptr, s32.ptr, s64.ptr,
+            dv.search_dataflow(self.shard, params, queries, g, N, e, self.inbox.ptr + b * self.q * 64,
+                               self.next_inbox.ptr + b * self.q * 64, ids.ptr, dists.ptr, s32.ptr, s64.ptr,
                                tuning=self.tuning, sm_limit=self.sm_limit, stream=self.stream)
         if timer is not None:
             e1.record(self.stream)

@@ -101,3 +101,51 @@ def test_multiprocess_dataflow_ring(tmp_path, world):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     report = json.loads(out.read_text())
     assert report and all(v == "ok" for v in report.values()), report
+
+
+# Opt-in path-extension knobs (not the reference's behaviour): top-F entries
+# forwarded per query and smaller budgets for stages >= 1.  The oracle runs
+# the same knobs (oracle.run(..., ext=...)), so the GPU paths must still agree
+# with it bit for bit -- through the stage schedule, the dataflow ring and pw_run.
+EXT = [dict(forward_count=2), dict(forward_count=4, late_l=64), dict(late_l=48, late_max_iter=6),
+       dict(forward_count=3, late_max_iter=8)]
+
+
+@pytest.mark.parametrize("n_shards", [2, 4])
+@pytest.mark.parametrize("arm", [0, 1, 2])
+@pytest.mark.parametrize("ext", range(len(EXT)))
+def test_extension_knobs_match_oracle(rings, n_shards, arm, ext):
+    queries, ctxs, shards = rings[n_shards]
+    params = SearchParams(**ARMS[arm])
+    knobs = EXT[ext]
+    want = oracle_dict(oracle.run(queries, ctxs, params, "pipelined", ext=knobs))
+    got = _run(queries, shards, params, tuning=dict(knobs), reps=2)
+    assert_same(got, want, f"dataflow ext={knobs} N={n_shards} arm={arm}")
+    # stage-synchronous schedule (N x N pw_search_stage launches)
+    q = queries.shape[0]
+    run = dv.DeviceRun(q, len(shards), params.k, "cuda")
+    dv.run_local(shards, params, torch.from_numpy(queries).cuda(), "pipelined", run, tuning=dict(knobs))
+    torch.cuda.synchronize()
+    got2 = run_dict(run.shard_ids.cpu().numpy(), run.shard_dists.cpu().numpy(), run.final_ids.cpu().numpy(),
+                    run.final_dists.cpu().numpy(), run.s32.cpu().numpy(), run.s64.cpu().numpy())
+    assert_same(got2, want, f"stages ext={knobs} N={n_shards} arm={arm}")
+    # the host API (pw_run, pinned host buffers) with the same knobs
+    import paper_2507_17094_b200 as pw
+    from golden_util import result_dict
+
+    got3 = result_dict(pw.run_pipelined(pw.Dataset(queries), None, None, params, contexts=ctxs,
+                                        tuning=dict(knobs)))
+    for key in ("final_ids", "final_dists", "shard_ids", "shard_dists"):
+        assert np.array_equal(got3[key], want[key]), (knobs, key)
+    assert np.array_equal(got3["comm"], want["comm"])
+
+
+def test_extension_knob_validation(rings):
+    queries, ctxs, shards = rings[2]
+    params = SearchParams(**ARMS[0])
+    q = torch.from_numpy(queries).cuda()
+    run = dv.DeviceRun(q.shape[0], 2, params.k, "cuda")
+    with pytest.raises(ValueError, match="forward_count"):
+        dv.run_local(shards, params, q, "pipelined", run, tuning={"forward_count": 11})
+    with pytest.raises(ValueError, match="k <= l"):
+        dv.run_local(shards, params, q, "pipelined", run, tuning={"late_l": 5})

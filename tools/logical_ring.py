@@ -34,6 +34,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--ns", default="2,4,8")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--ext", action="store_true",
+                help="also search the opt-in path-extension knobs (forward_count, late-stage l / max_iter)")
+ap.add_argument("--pw-grid", default="", help="restrict the parity-mode grid, e.g. 0.75:1,0.8:1")
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
 dev = torch.device("cuda", 0)
@@ -68,11 +71,11 @@ for N in (int(x) for x in args.ns.split(",")):
     run = dv.DeviceRun(q.shape[0], N, k, dev)
     df = dv.LocalDataflow(shards, q.shape[0], k, dev)
 
-    def recall(p, how):
+    def recall(p, how, tn=tuning):
         if how == "dataflow":
-            df.run(p, q, run, tuning=tuning)
+            df.run(p, q, run, tuning=tn)
         else:
-            dv.run_local(shards, p, q, how, run, tuning=tuning)
+            dv.run_local(shards, p, q, how, run, tuning=tn)
         torch.cuda.synchronize()
         return builder.recall_at_k(run.final_ids.cpu().numpy(), truth, bench.RECALL_AT)
 
@@ -87,7 +90,10 @@ for N in (int(x) for x in args.ns.split(",")):
                     "ms": round(timed(lambda: dv.run_local(shards, p, q, "baseline", run, tuning=tuning)), 3)}
     best = None
     for how in ("pipelined", "dataflow"):
-        for dr, gi in bench.PW_GRID:
+        grid = [tuple(float(v) for v in x.split(":")) for x in args.pw_grid.split(",")] if args.pw_grid \
+            else bench.PW_GRID
+        for dr, gi in grid:
+            gi = int(gi)
             for l in bench.L_GRID:
                 pp = bench.arm_params("pathweaver", l, k, discard=dr, ghost_iter=gi)
                 rec = recall(pp, how)
@@ -105,6 +111,38 @@ for N in (int(x) for x in args.ns.split(",")):
                 best = cand
     out["pathweaver"] = best
     out["pw_over_naive"] = round(out["naive"]["ms"] / best["ms"], 3) if best else None
+    if args.ext and best:
+        # opt-in knobs beyond the reference (results differ from it): forward
+        # the top-F entries, smaller queue / iteration budget
+        # for stages >= 1 (SPEC.md per-stage budget vector); dataflow ring,
+        # the best parity-mode (discard, ghost_max_iter)
+        ext = []
+        for F in (1, 2, 4):
+            for frac in (1.0, 0.75, 0.5):
+                for lmi in (0, 16, 8):
+                    if F == 1 and frac == 1.0 and lmi == 0:
+                        continue
+                    hit = None
+                    for l in bench.L_GRID:
+                        ll = max(k, int(round(l * frac / 16)) * 16) if frac < 1 else 0
+                        tn = dict(tuning, forward_count=F, late_l=ll, late_max_iter=lmi)
+                        pp = bench.arm_params("pathweaver", l, k, discard=best["discard"],
+                                              ghost_iter=best["ghost_max_iter"])
+                        rec = recall(pp, "dataflow", tn)
+                        if rec >= 0.95:
+                            hit = (l, ll, rec, tn, pp)
+                            break
+                    if hit is None:
+                        continue
+                    l, ll, rec, tn, pp = hit
+                    ms = timed(lambda: df.run(pp, q, run, tuning=tn))
+                    ext.append({"forward_count": F, "l": l, "late_l": ll or l, "late_max_iter": lmi or 64,
+                                "recall": round(rec, 4), "ms": round(ms, 3)})
+        ext.sort(key=lambda e: e["ms"])
+        out["extension_grid"] = ext
+        if ext:
+            out["extension_best"] = ext[0]
+            out["ext_over_naive"] = round(out["naive"]["ms"] / ext[0]["ms"], 3)
     out["projected_qps_n_gpus"] = {
         "naive": round(q.shape[0] / (out["naive"]["ms"] / N) * 1e3),
         "pathweaver": round(q.shape[0] / (best["ms"] / N) * 1e3) if best else None}
