@@ -20,6 +20,8 @@
 #pragma once
 #include <stdint.h>
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors built on the host)
+
 #include "rng_pcg64.cuh"
 
 #ifndef PW_MAX_THREADS
@@ -67,6 +69,12 @@ struct TaskRecord {         // per-task outputs of pw_search_one
 };
 
 struct KArgs {
+    // TMA descriptors of the vector rows (main graph, ghost graph) for the
+    // tile::gather4 scoring path (tma_rows): 2D {d, n} tensors, box {spad, 1}
+    // -- the box is wider than a row, so columns d..spad-1 are zero-filled
+    // out of bounds and the rows land at the padded, bank-conflict-free
+    // staging stride without any extra traffic
+    CUtensorMap tm_main, tm_ghost;
     GraphDev main, ghost;
     const int32_t* inter;   // (n,) or null
     int32_t d, W;
@@ -106,6 +114,7 @@ struct KArgs {
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
         o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
+    int32_t tma_rows;       // scoring rows by TMA tile::gather4 (tuning flag 8)
     int32_t bulk_adj;       // expansion rows 16-byte aligned: 1 cp.async x16, 2 TMA bulk (flag 4)
     int32_t prefetch;       // L2-prefetch predicted parent rows
     unsigned long long* phase;  // per-phase cycle totals (PW_PHASE_TIMERS builds only)
@@ -265,6 +274,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// elect.sync: one lane of the warp; ptxas knows the region is single-threaded,
+// so per-lane values feed TMA's uniform operands with a plain R2UR (an
+// `if (lane == 0)` region makes it emit a lane waterfall instead)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n" : "=r"(pred));
+    return pred != 0;
+}
+// TMA tile::gather4: 4 rows (row coordinates r0..r3, -1 = out of bounds,
+// zero-filled, no traffic) x box columns from column 0 into dst, completing
+// on bar (SASS UTMALDG.2D.GATHER4)
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int32_t r0, int32_t r1, int32_t r2,
+                                            int32_t r3, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
 }
 
@@ -929,8 +958,29 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
         // the ghost graph's rows are reused by every query: not streaming
         const uint64_t pol = (PW_EVICT_LAST && G.vec == A.ghost.vec) ? l2_evict_last_policy()
                                                                      : l2_evict_first_policy();
+        const bool tma = A.tma_rows != 0;
+        const CUtensorMap* tm = G.vec == A.ghost.vec ? &A.tm_ghost : &A.tm_main;
+        if (tma) fence_proxy_async();  // the ring was last written / read by the generic proxy
         auto issue = [&](int g) {
-            if (g < ngroups) {
+            if (g < ngroups && tma) {
+                // one elected lane: ceil(rows / 4) gather4 copies into half g & 1
+                const int r0 = g * RH;
+                const int rows = min(RH, n - r0);
+                VT* dst0 = reinterpret_cast<VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
+                uint64_t* bar = S.mbar + (g & 1);
+                if (elect_one()) {
+                    const int n4 = (rows + 3) >> 2;
+                    mbar_arrive_expect(bar, (uint32_t)(n4 * 4 * sp * (int)sizeof(VT)));
+#pragma unroll 1
+                    for (int i = 0; i < n4; i++) {
+                        const int b = r0 + 4 * i;
+                        const int c = rows - 4 * i;
+                        tma_gather4(dst0 + (size_t)(4 * i) * sp, tm, S.newl[b], c > 1 ? S.newl[b + 1] : -1,
+                                    c > 2 ? S.newl[b + 2] : -1, c > 3 ? S.newl[b + 3] : -1, bar, pol);
+                    }
+                }
+                __syncwarp();
+            } else if (g < ngroups) {
                 const int r0 = g * RH;
                 const int rows = min(RH, n - r0);
                 VT* dst0 = reinterpret_cast<VT*>(S.stage) + (size_t)(g & 1) * RH * sp;
@@ -979,10 +1029,35 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
             ns += __popc(b);
         };
-        issue(0);
-        issue(1);
-        for (int g = 0; g < ngroups; g++) {
-            cp_wait<1>();
+        // g = -2, -1 only issue (the two halves in flight): ONE inlined copy
+        // of the issue code (instruction-cache footprint)
+#pragma unroll 1
+        for (int g = -2; g < ngroups; g++) {
+            if (g < 0) {
+                issue(g + 2);
+                continue;
+            }
+            if (tma) {
+                // bounded (~seconds): a transaction count that never completes
+                // raises (flag 32) instead of hanging the GPU
+                const uint32_t par = (S.phase >> (g & 1)) & 1u;
+                uint32_t done = 0;
+                for (uint32_t spin = 0; !done; spin++) {
+                    asm volatile(
+                        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                        " selp.u32 %0, 1, 0, p;\n}\n"
+                        : "=r"(done)
+                        : "r"(smem_u32(S.mbar + (g & 1))), "r"(par)
+                        : "memory");
+                    if (!done && spin > (1u << 22)) {
+                        atomicOr(A.err, 32);
+                        break;
+                    }
+                }
+                S.phase ^= 1u << (g & 1);
+            } else {
+                cp_wait<1>();
+            }
             __syncwarp();
             const int r0 = g * RH;
             const int rows = min(RH, n - r0);
@@ -1001,9 +1076,10 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
                 emit(r0 + pass, min(8, rows - pass), dist);
             }
             __syncwarp();
+            if (tma) fence_proxy_async();  // generic reads of this half before the async overwrite
             issue(g + 2);
         }
-        cp_wait<0>();
+        if (!tma) cp_wait<0>();
         __syncwarp();
     } else {
         const int row_bytes = A.d * (int)sizeof(VT);

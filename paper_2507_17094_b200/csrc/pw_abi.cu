@@ -422,6 +422,40 @@ __global__ void l2_pairs_kernel(const float* __restrict__ a, const float* __rest
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+// 2D {d, n} row tensor with a {box_w, 1} box (box_w >= d: the extra columns
+// are out of bounds, zero-filled, so rows land at stride box_w) for gather4
+int make_row_tensor_map(CUtensorMap* tm, const void* base, int64_t n, int32_t d, int32_t elem, int32_t box_w) {
+    EncodeTiledFn fn = encode_tiled();
+    if (!fn) return set_err(PW_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)std::max<int64_t>(n, 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)d * (cuuint64_t)elem};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, 1u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = fn(tm, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 2,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(PW_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return 0;
+}
+
 SearchCfg make_cfg(const pw_params& p, int64_t n, int32_t j) {
     SearchCfg c;
     c.k = p.k;
@@ -684,6 +718,16 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // TMA bulk copies need 16-byte sizes/alignment for every expansion row kind
     auto b16 = [](int64_t bytes) { return bytes % 16 == 0; };
     A.bulk_rows = 0;
+    // TMA tile::gather4 scoring rows (tuning flag 8): specialised kernels whose
+    // padded staging row fits one box (<= 256 elements) and whose global row
+    // stride is a 16-byte multiple
+    A.tma_rows = 0;
+    if (tun && (tun->flags & 8) && specialised && A.spad <= 256 && ((int64_t)d * elem) % 16 == 0 &&
+        ((int64_t)A.spad * elem) % 16 == 0) {
+        if ((rc = make_row_tensor_map(&A.tm_main, sh->vec, sh->n, d, elem, A.spad))) return rc;
+        if (sh->gn > 0 && (rc = make_row_tensor_map(&A.tm_ghost, sh->gvec, sh->gn, d, elem, A.spad))) return rc;
+        A.tma_rows = 1;
+    }
     A.prefetch = (tun && (tun->flags & 1)) ? 1 : 0;
     A.bulk_adj = (b16(4ll * G.j) && (!ghost_on || b16(4ll * sh->gj)) &&
                   (A.cfg.prune_sel != PW_SEL_DIRECTION || (b16((int64_t)elem * d) && b16(4ll * G.j * W))))
@@ -775,8 +819,9 @@ int check_err(pw_shard* sh) {
     PW_CUDA(cudaMemcpy(&e, sh->counter + 1, sizeof e, cudaMemcpyDeviceToHost));
     if (e) {
         cudaMemset(sh->counter + 1, 0, sizeof(int32_t));
-        return set_err(PW_ECUDA, (e & 16) ? std::string("dataflow inbox wait timed out (flag ") + std::to_string(e) + ")"
-                                          : "beam_search_kernel internal table overflow (flag " + std::to_string(e) + ")");
+        return set_err(PW_ECUDA, (e & 16)   ? std::string("dataflow inbox wait timed out (flag ") + std::to_string(e) + ")"
+                                 : (e & 32) ? std::string("TMA gather never completed (flag ") + std::to_string(e) + ")"
+                                            : "beam_search_kernel internal table overflow (flag " + std::to_string(e) + ")");
     }
     return 0;
 }

@@ -338,3 +338,18 @@ def test_initial_batch_choice_tail_shuffle(synth, mode, m, seed_mode):
     got = result_dict(runner(pw.Dataset(queries[:200]), None, None, params, contexts=ctxs))
     want = oracle_dict(oracle.run(queries[:200], ctxs, params, mode))
     assert_run_equal(got, want, f"choice tail m={m} {seed_mode} {mode}")
+
+
+@pytest.mark.parametrize("d", [96, 128, 200, 960])
+@pytest.mark.parametrize("arm", range(len(SYNTH_ARMS)))
+@pytest.mark.parametrize("mode", ["baseline", "pipelined"])
+@pytest.mark.parametrize("flags", [8, 10])
+def test_tma_gather4_rows_match_oracle(synth, d, arm, mode, flags):
+    """Scoring rows staged by TMA tile::gather4 (tuning flag 8; d = 960 rows
+    do not fit one box and keep the cp.async path): same results."""
+    queries, ctxs = synth[d]
+    params = SearchParams(**SYNTH_ARMS[arm])
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    got = result_dict(runner(pw.Dataset(queries), None, None, params, contexts=ctxs, tuning={"flags": flags}))
+    want = oracle_dict(oracle.run(queries, ctxs, params, mode))
+    (assert_run_equal_lossy if flags & 2 else assert_run_equal)(got, want, f"tma d={d} arm={arm} {mode}")

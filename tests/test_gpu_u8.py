@@ -111,3 +111,17 @@ def test_u8_rows_nonintegral_queries_match_oracle(u8sets, d, shift):
             got = result_dict(runner(pw.Dataset(q), None, None, params, contexts=ctxs))
             want = oracle_dict(oracle.run(q, ctxs, params, mode))
             assert_run_equal(got, want, f"u8 {shift} d={d} arm={arm} {mode}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [128, 96])
+@pytest.mark.parametrize("arm", range(len(ARMS)))
+@pytest.mark.parametrize("flags", [8, 10])
+def test_u8_rows_tma_gather4_match_oracle(u8sets, d, arm, flags):
+    """Scoring rows by TMA tile::gather4 (tuning flag 8) on uint8 rows."""
+    queries, ctxs = u8sets[d]
+    params = SearchParams(**ARMS[arm])
+    got = result_dict(pw.run_pipelined(pw.Dataset(queries), None, None, params, contexts=ctxs,
+                                       tuning={"flags": flags}))
+    want = oracle_dict(oracle.run(queries, ctxs, params, "pipelined"))
+    (assert_run_equal_lossy if flags & 2 else assert_run_equal)(got, want, f"u8 tma d={d} arm={arm}")

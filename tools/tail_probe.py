@@ -19,15 +19,18 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--l", type=int, default=256)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--discard", type=float, default=0.75)
+ap.add_argument("--ghost-iter", type=int, default=1)
+ap.add_argument("--tuning", default='{"flags": 2}')
 args = ap.parse_args()
 cfg = bench.CONFIGS[args.config]
-tuning = {"flags": 2}
+tuning = json.loads(args.tuning)
 W = bench.build_workload(cfg, 0, 1, torch.device("cuda", 0))
 gh = W["ghost"] or (None, None)
 shard = dv.TensorShard(W["vec"], W["adj"], W["rows"].to(torch.int32), W["direction"], None, gh[0], gh[1])
 q_all = W["queries"]
 for arm, mode in (("pathweaver", "pipelined"), ("naive", "baseline")):
-    p = bench.arm_params(arm, args.l, cfg["k"])
+    p = bench.arm_params(arm, args.l, cfg["k"], discard=args.discard, ghost_iter=args.ghost_iter)
     lc = _abi.launch_config(shard.handle, p, tuning)
     warps = lc["warps_per_sm"] * lc["blocks"]
     for mult in (1, 2, 3, 4, None, 8):
