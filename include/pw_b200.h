@@ -206,6 +206,19 @@ int pw_search_dataflow(pw_shard* shard, const pw_params* params, const pw_tuning
 int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, const int64_t* ib,
                 int64_t n, float* out, void* stream);
 
+/* K4 tensor-core kNN screen (replaces the distance screen of
+ * graphs.py:65-78 `_knn_block`, which keeps k + 8 candidates per row by a
+ * GEMM-style distance before the exact rescore): for each of the nq query
+ * rows q (device, (nq, d) f32), the kc base rows x (device, (n, d) f32) with
+ * the smallest approximate |x_c|^2 - 2 q.x_c (TF32 tensor cores, FP32
+ * accumulation; xn = |x_c|^2, (n,) f32), query row r excluding base row
+ * r + self_off when self_off >= 0.  Outputs (nq, kc) int32 ids / f32 values,
+ * unsorted, -1 / +inf when n - 1 < kc.  d % 4 == 0, kc <= 64.  The values only
+ * select candidates: exact.py rescores them bit-exactly and certifies each
+ * row against the TF32 error bound. */
+int pw_knn_screen(const float* q, int64_t nq, const float* x, int64_t n, int32_t d, const float* xn,
+                  int64_t self_off, int32_t kc, int32_t* out_ids, float* out_vals, void* stream);
+
 /* Validate a shard's inter_map (pipeline.py:339 forwards inter_map[top1]
  * as the next shard's entry) against the next shard's size n_next: every
  * value must be in [0, n_next).  Synchronous once per (shard, n_next);

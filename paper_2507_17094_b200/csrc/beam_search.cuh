@@ -80,8 +80,10 @@ struct KArgs {
     int32_t d, W;
     int32_t spad;           // staging row stride in elements (bank-conflict-free passes)
     L2Plan plan;
-    SearchCfg cfg, gcfg;
-    SearchCfg cfg_late;     // stages >= 1 when has_late (opt-in per-stage budgets)
+    // consecutive: a task's config is (&cfg)[0 main | 1 stages >= 1 | 2 ghost]
+    SearchCfg cfg;
+    SearchCfg cfg_late;     // stages >= 1 (== cfg unless opt-in per-stage budgets)
+    SearchCfg gcfg;
     int32_t has_late;
     int32_t fwd;            // entries forwarded per query (1 = the reference)
     int32_t ghost_on;       // run the ghost prologue when the task has no entry
@@ -277,6 +279,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// TMA tile::gather4 scoring path (tuning flag 8).  Off in the product build:
+// measured at the C2 bench point (profiles/r02/ab_tma_r02m.log) the gather4
+// path is slower than LDGSTS (PW 1.62 vs 1.52 ms, naive 3.22 vs 2.88 ms) and
+// merely compiling it in costs 3-5% (code size / registers in the hot loop);
+// build with -DPW_TMA_ROWS=1 for the A/B (tests pass either way).
+#ifndef PW_TMA_ROWS
+#define PW_TMA_ROWS 0
+#endif
 // elect.sync: one lane of the warp; ptxas knows the region is single-threaded,
 // so per-lane values feed TMA's uniform operands with a plain R2UR (an
 // `if (lane == 0)` region makes it emit a lane waterfall instead)
@@ -958,7 +968,7 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
         // the ghost graph's rows are reused by every query: not streaming
         const uint64_t pol = (PW_EVICT_LAST && G.vec == A.ghost.vec) ? l2_evict_last_policy()
                                                                      : l2_evict_first_policy();
-        const bool tma = A.tma_rows != 0;
+        const bool tma = PW_TMA_ROWS && A.tma_rows != 0;
         const CUtensorMap* tm = G.vec == A.ghost.vec ? &A.tm_ghost : &A.tm_main;
         if (tma) fence_proxy_async();  // the ring was last written / read by the generic proxy
         auto issue = [&](int g) {
@@ -1029,14 +1039,10 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             if (surv) S.ckey[ns + __popc(b & lanemask_lt())] = key;
             ns += __popc(b);
         };
-        // g = -2, -1 only issue (the two halves in flight): ONE inlined copy
-        // of the issue code (instruction-cache footprint)
-#pragma unroll 1
-        for (int g = -2; g < ngroups; g++) {
-            if (g < 0) {
-                issue(g + 2);
-                continue;
-            }
+        issue(0);
+        issue(1);
+        for (int g = 0; g < ngroups; g++) {
+#if PW_TMA_ROWS
             if (tma) {
                 // bounded (~seconds): a transaction count that never completes
                 // raises (flag 32) instead of hanging the GPU
@@ -1055,7 +1061,9 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
                     }
                 }
                 S.phase ^= 1u << (g & 1);
-            } else {
+            } else
+#endif
+            {
                 cp_wait<1>();
             }
             __syncwarp();
@@ -1767,7 +1775,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
 
 template <int D, typename VT, int M>
 __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;
     const int gwarp = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -1923,8 +1931,7 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
                 rng = A.rng_io ? A.rng_io[task]
                                : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)tsk[0], (uint64_t)tsk[1]));
             }
-            converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G,
-                                             gph ? A.gcfg : (A.has_late && tsk[1] > 0 ? A.cfg_late : A.cfg),
+            converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G, (&A.cfg)[gph ? 2 : (tsk[1] > 0 ? 1 : 0)],
                                              ns, fill_random, rng, task, &n_logged);
             if (gph) {
                 if (lane == 0) S.cand[0] = A.ghost.gid[(uint32_t)S.qk_cur()[0]];

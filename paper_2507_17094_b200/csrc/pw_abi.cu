@@ -538,10 +538,14 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     if (tun && tun->late_l > 0) lp.l = tun->late_l;
     if (tun && tun->late_max_iter > 0) lp.max_iter = tun->late_max_iter;
     A.has_late = (lp.l != p.l || lp.max_iter != p.max_iter) ? 1 : 0;
+    A.cfg_late = A.cfg;
     if (A.has_late) {
         if ((rc = validate_params(lp))) return rc;
         A.cfg_late = make_cfg(lp, G.n, G.j);
     }
+    static_assert(offsetof(KArgs, cfg_late) == offsetof(KArgs, cfg) + sizeof(SearchCfg) &&
+                      offsetof(KArgs, gcfg) == offsetof(KArgs, cfg) + 2 * sizeof(SearchCfg),
+                  "K1 indexes (&cfg)[0..2]");
     const int32_t Lq = std::max(p.l, lp.l);  // queue capacity (smem layout)
     A.ghost_on = ghost_on ? 1 : 0;
     A.seed_mode = p.seed_mode;
@@ -551,6 +555,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         return set_err(PW_EINVAL, "direction table required for direction-guided selection");
 
     // ---- shared-memory layout per warp
+    const bool want_tma = PW_TMA_ROWS && tun && (tun->flags & 8);
     const int jm = std::max(G.j, ghost_on ? sh->gj : 0);
     const int d = sh->d;
     const int elem = sh->dtype == PW_DTYPE_U8 ? 1 : 4;  // bytes per vector element
@@ -667,6 +672,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         A.o_cand = (int32_t)(off + 4 * ckey_n);
         off = al(off + 8 * ckey_n);
         A.o_vh = (int32_t)off; off = al(off + 4 * H);
+        if (want_tma) off = (off + 127) / 128 * 128;  // TMA destinations: 128-byte aligned
         A.o_stage = (int32_t)off;
         A.o_bhk = (int32_t)off;
         A.o_bhp = (int32_t)(off + 4 * (int64_t)A.BH);
@@ -690,6 +696,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
             A.o_desc = (int32_t)off;
             off = al(off + 16 * n_desc);
         }
+        if (want_tma) off = (off + 127) / 128 * 128;
         A.warp_bytes = (int32_t)off;
         return off;
     };
@@ -722,8 +729,10 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // padded staging row fits one box (<= 256 elements) and whose global row
     // stride is a 16-byte multiple
     A.tma_rows = 0;
-    if (tun && (tun->flags & 8) && specialised && A.spad <= 256 && ((int64_t)d * elem) % 16 == 0 &&
-        ((int64_t)A.spad * elem) % 16 == 0) {
+    // every gather4 destination (half base + 4-row groups) 128-byte aligned
+    const int64_t row_b = (int64_t)A.spad * elem;
+    if (want_tma && specialised && A.spad <= 256 && ((int64_t)d * elem) % 16 == 0 && (4 * row_b) % 128 == 0 &&
+        ((int64_t)(A.R / 2) * row_b) % 128 == 0 && A.o_stage % 128 == 0 && A.warp_bytes % 128 == 0) {
         if ((rc = make_row_tensor_map(&A.tm_main, sh->vec, sh->n, d, elem, A.spad))) return rc;
         if (sh->gn > 0 && (rc = make_row_tensor_map(&A.tm_ghost, sh->gvec, sh->gn, d, elem, A.spad))) return rc;
         A.tma_rows = 1;
@@ -1046,6 +1055,18 @@ int pw_shard_check(pw_shard* sh) {
     if (!sh->counter) return 0;
     PW_CUDA(cudaSetDevice(sh->device));
     return check_err(sh);
+}
+
+extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, int64_t n, int32_t d,
+                                  const float* xn, int64_t self_off, int32_t kc, int32_t* out_ids,
+                                  float* out_vals, void* stream, char* msg);
+
+int pw_knn_screen(const float* q, int64_t nq, const float* x, int64_t n, int32_t d, const float* xn,
+                  int64_t self_off, int32_t kc, int32_t* out_ids, float* out_vals, void* stream) {
+    char msg[256] = {0};
+    const int rc = pw_knn_screen_impl(q, nq, x, n, d, xn, self_off, kc, out_ids, out_vals, stream, msg);
+    if (rc) return set_err(rc == -1 ? PW_EINVAL : PW_ECUDA, msg);
+    return 0;
 }
 
 int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, const int64_t* ib, int64_t n,

@@ -89,18 +89,109 @@ def _screen(base: torch.Tensor, queries: torch.Tensor, kk: int, qchunk: int = 40
     return out
 
 
-def exact_topk(base: torch.Tensor, queries: torch.Tensor, k: int, exclude_self: bool = False,
-               pad: int = PAD) -> tuple[torch.Tensor, torch.Tensor]:
-    """k best rows of ``base`` per query by (exact squared L2, id): screen,
-    bit-exact rescore, rank.  exclude_self: query i is base row i."""
-    nq = queries.shape[0]
-    cand = _screen(base, queries, k + pad + (1 if exclude_self else 0))
-    c = cand.shape[1]
+# K4 (csrc/knn_screen.cu) above this many screened pairs; below, the FP32
+# GEMM screen is fast enough and needs no certification
+TC_MIN_PAIRS = 1 << 30
+TC_ERR = 2.0 ** -7.5   # |TF32 dot - exact| <= TC_ERR/2 * |q| |x| (generous; exact.py _certify)
+
+
+def knn_screen_tc(base: torch.Tensor, queries: torch.Tensor, kc: int, self_off: int = -1):
+    """K4 tensor-core screen: (nq, kc) int64 candidate ids (-1 = none) and
+    their approximate |x|^2 - 2 q.x (TF32 operands, FP32 accumulation),
+    unsorted; query row r skips base row r + self_off when self_off >= 0."""
+    lib = _abi.load()
+    base = base.contiguous().float()
+    queries = queries.contiguous().float()
+    nq, n, d = queries.shape[0], base.shape[0], base.shape[1]
+    xn = (base * base).sum(1)
+    ids = torch.empty((nq, kc), dtype=torch.int32, device=base.device)
+    vals = torch.empty((nq, kc), dtype=torch.float32, device=base.device)
+    st = torch.cuda.current_stream(base.device).cuda_stream
+    _abi.check(lib.pw_knn_screen(queries.data_ptr(), nq, base.data_ptr(), n, d, xn.data_ptr(), int(self_off),
+                                 kc, ids.data_ptr(), vals.data_ptr(), C.c_void_p(st)))
+    return ids.to(torch.int64), vals, xn
+
+
+def _certify(queries: torch.Tensor, base_norm_max: float, vals: torch.Tensor, kth_exact: torch.Tensor,
+             full: torch.Tensor) -> torch.Tensor:
+    """Rows whose exact top-k provably lies inside the screened candidates.
+
+    Every non-candidate c has a screened value a_c >= tau (the list's worst),
+    and |a_c - t_c| <= E with t_c = |x_c|^2 - 2 q.x_c in exact arithmetic.
+    Columns with |x_c| > R = |q| + sqrt(D_k) + 1e-3 are farther than D_k (the
+    k-th exact distance) by the triangle inequality; for the others E <=
+    TC_ERR |q| R + 2^-15 (2 R^2 + 2 |q| R).  The f32 pairwise distance is
+    within 2^-20 relative of the real one.  So if (|q|^2 + tau - E)(1 - 2^-20)
+    > D_k, no non-candidate can enter the top k (strictly: no id tie-break
+    can either)."""
+    q64 = queries.double()
+    qn2 = (q64 * q64).sum(1)
+    qn = qn2.sqrt()
+    tau = torch.where(torch.isfinite(vals), vals, torch.full_like(vals, -float("inf"))).max(1).values.double()
+    dk = kth_exact.double()
+    R = torch.clamp(qn + dk.clamp(min=0).sqrt() + 1e-3, max=float(base_norm_max) + 1e-3)
+    E = TC_ERR * qn * R + 2.0 ** -15 * (2 * R * R + 2 * qn * R)
+    ok = (qn2 + tau - E) * (1 - 2.0 ** -20) > dk * (1 + 2.0 ** -20)
+    return ok | ~full  # a list that is not full holds every other row
+
+
+def _rescore_rank(base, queries, cand, k, exclude_self):
+    """Bit-exact rescore (pw_l2_pairs) + (distance, id) rank of candidates."""
+    nq, c = cand.shape
+    valid = cand >= 0
+    cc = torch.where(valid, cand, torch.zeros_like(cand))
     qi = torch.arange(nq, device=base.device).repeat_interleave(c)
-    sq = l2_pairs(queries, base, qi, cand.reshape(-1)).reshape(nq, c)
+    sq = l2_pairs(queries, base, qi, cc.reshape(-1)).reshape(nq, c)
+    bad = ~valid
     if exclude_self:
-        sq = torch.where(cand == torch.arange(nq, device=base.device)[:, None],
-                         torch.full_like(sq, float("inf")), sq)
+        bad |= cand == torch.arange(nq, device=base.device)[:, None]
+    sq = torch.where(bad, torch.full_like(sq, float("inf")), sq)
+    key = _rank_keys(sq, torch.where(valid, cand, torch.full_like(cand, (1 << 31) - 1)))
+    order = torch.sort(key, dim=1).indices[:, :k]
+    return torch.gather(cand, 1, order), torch.gather(sq, 1, order)
+
+
+def exact_topk(base: torch.Tensor, queries: torch.Tensor, k: int, exclude_self: bool = False,
+               pad: int = PAD, screen: str = "auto", stats: dict | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """k best rows of ``base`` per query by (exact squared L2, id): screen,
+    bit-exact rescore, rank.  exclude_self: query i is base row i.
+
+    screen: "fp32" (blocked FP32 GEMM + top-k), "tc" (K4 tensor-core screen,
+    each row certified against the TF32 error bound; uncertified rows are
+    redone by the FP32 screen), "auto" (tc for large problems)."""
+    nq, n, d = queries.shape[0], base.shape[0], base.shape[1]
+    kc = k + pad + (1 if exclude_self else 0)
+    use_tc = screen == "tc" or (screen == "auto" and nq * n >= TC_MIN_PAIRS and kc <= 64 and d % 4 == 0
+                                and d <= 256)
+    if not use_tc:
+        cand = _screen(base, queries, kc)
+        return _rescore_rank(base, queries, cand, k, exclude_self)
+    kc = min(64, max(kc, k + 16))
+    cand, vals, xn = knn_screen_tc(base, queries, kc, 0 if exclude_self else -1)
+    ids, sq = _rescore_rank(base, queries, cand, k, exclude_self)
+    full = (cand >= 0).all(1)
+    ok = _certify(queries, float(xn.max().sqrt()), vals, sq[:, k - 1], full)
+    redo = torch.nonzero(~ok).flatten()
+    if stats is not None:
+        stats.update(rows=nq, certified=int(ok.sum()), redone=int(redo.numel()), kc=kc)
+    if redo.numel():
+        # FP32 screen for the uncertified rows (exclude_self: those rows'
+        # own index in base is their query index)
+        qs = queries[redo].contiguous()
+        c2 = _screen(base, qs, k + pad + (1 if exclude_self else 0))
+        i2, s2 = _rescore_rank(base, qs, c2, k, False) if not exclude_self else \
+            _rescore_rank_self(base, qs, c2, k, redo)
+        ids[redo] = i2
+        sq[redo] = s2
+    return ids, sq
+
+
+def _rescore_rank_self(base, qs, cand, k, rows):
+    """_rescore_rank for a subset of query rows that are base rows `rows`."""
+    nq, c = cand.shape
+    qi = torch.arange(nq, device=base.device).repeat_interleave(c)
+    sq = l2_pairs(qs, base, qi, cand.reshape(-1)).reshape(nq, c)
+    sq = torch.where(cand == rows[:, None], torch.full_like(sq, float("inf")), sq)
     key = _rank_keys(sq, cand)
     order = torch.sort(key, dim=1).indices[:, :k]
     return torch.gather(cand, 1, order), torch.gather(sq, 1, order)

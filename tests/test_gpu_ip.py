@@ -81,3 +81,75 @@ def test_ip_top1_is_max_inner_product(ipsets):
     params = SearchParams(k=5, l=300, m=300, r=1, max_iter=3, seed=1, metric="ip")
     res = pw.search(q, ctx, params, rng=stream(1, TAG_SEARCH, 0, 0))
     assert res.ids[0] == int(np.argmax(x @ q))
+
+
+# ---- independent pin of the IP metric against float64 brute force (not the
+# oracle's float32 restatement): north_star's acceptance rule -- ids identical
+# except where distances tie within 1e-5 relative -- at the C5 shape (d = 200,
+# k = 100) on exhaustive searches, and the arithmetic of every returned
+# distance on a real graph.
+
+def _f64_neg_ip(x, q):
+    return -(x.astype(np.float64) @ q.astype(np.float64))
+
+
+def _assert_ids_equal_up_to_ties(ids, dists64_of_ids, truth_ids, truth_d64, what):
+    """Position by position: same id, or both ids' float64 distances tie with
+    the truth's within 1e-5 relative."""
+    for p in range(len(truth_ids)):
+        if ids[p] == truth_ids[p]:
+            continue
+        a, b = dists64_of_ids[p], truth_d64[p]
+        assert abs(a - b) <= 1e-5 * max(abs(a), abs(b)) + 1e-6, (what, p, ids[p], truth_ids[p], a, b)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_ip_exhaustive_matches_float64_bruteforce_c5_shape(seed):
+    """Complete graph over 400 Text2Image-shaped rows (d = 200), k = 100,
+    l >= n: the search scores every row, so its top 100 must be the float64
+    brute-force top 100 (ties within 1e-5 excepted) and every returned
+    distance must equal -(q . x) in float64 to 1e-5 relative."""
+    n, d, k = 400, 200, 100
+    x = unit_rows(n, d, seed=100 + seed)
+    qs = unit_rows(8, d, seed=200 + seed)
+    adj = np.array([[(i + 1 + t) % n for t in range(n - 1)] for i in range(n)], np.int32)
+    ctx = pw.ShardContext(vectors=x, adj=adj[:, :n - 1], global_ids=np.arange(n, dtype=np.int32))
+    params = SearchParams(k=k, l=n, m=n, r=1, max_iter=3, seed=seed, metric="ip")
+    for qi, q in enumerate(qs):
+        res = pw.search(q, ctx, params, rng=stream(seed, TAG_SEARCH, qi, 0))
+        d64 = _f64_neg_ip(x, q)
+        order = np.lexsort((np.arange(n), d64))[:k]
+        got_d64 = d64[res.ids]
+        # 1e-5 relative, plus an absolute 1e-6 floor for sums near zero (unit
+        # rows: sum |x_i q_i| <= 1, float32 pairwise-sum error < 1e-6)
+        assert np.all(np.abs(res.dists.astype(np.float64) - got_d64) <= 1e-5 * np.abs(got_d64) + 1e-6)
+        _assert_ids_equal_up_to_ties(res.ids, got_d64, order, d64[order], f"seed {seed} q {qi}")
+
+
+def test_ip_graph_search_distances_and_ranks_float64():
+    """C5-shaped run on a real graph (8000 x 200, k = 100, pipelined, DGS +
+    ghost): every returned distance equals float64 -(q . x) to 1e-5 relative,
+    lists are ranked by float64 distance up to 1e-5 ties, and recall@10
+    against the float64 brute-force truth is high."""
+    n, d, nq, k = 8000, 200, 200, 100
+    xall = unit_rows(n + nq, d, seed=77)
+    x, q = xall[:n], np.ascontiguousarray(xall[n:])
+    ctxs = make_contexts(x, 2, 32, seed=7)
+    params = SearchParams(k=k, l=160, m=64, r=8, max_iter=64, seed=3, selection="direction",
+                          discard_ratio=0.5, cooldown_ratio=0.3, ghost_enabled=True, ghost_max_iter=4,
+                          metric="ip")
+    res = pw.run_pipelined(pw.Dataset(q), None, None, params, contexts=ctxs)
+    s64 = -(q.astype(np.float64) @ x.astype(np.float64).T)          # (nq, n)
+    truth = np.argsort(s64, axis=1, kind="stable")[:, :10]
+    hits = 0
+    for i in range(nq):
+        ids = res.final_ids[i]
+        ok = ids >= 0
+        got64 = s64[i, ids[ok]]
+        assert np.all(np.abs(res.final_dists[i][ok].astype(np.float64) - got64)
+                      <= 1e-5 * np.abs(got64) + 1e-6), i
+        # ranked: float64 order agrees except within 1e-5 relative ties
+        dd = np.diff(got64)
+        assert np.all(dd >= -(1e-5 * np.abs(got64[1:]) + 1e-6)), i
+        hits += len(set(ids[:10].tolist()) & set(truth[i].tolist()))
+    assert hits / (10 * nq) >= 0.95
