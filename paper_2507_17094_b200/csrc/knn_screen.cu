@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <cstdio>
+#include <cstdlib>
 
 namespace knn {
 
@@ -38,7 +39,8 @@ struct Args {
     const float* xn;           // (n,) |x_c|^2
     int32_t* out_ids;          // (nq, kc)
     float* out_vals;           // (nq, kc)
-    uint32_t o_b, o_bar, o_lv, o_li, o_tmem;  // shared-memory offsets
+    uint32_t o_b, o_bar, o_lv, o_li, o_tmem, o_nb, o_scr;  // shared-memory offsets
+    int32_t debug;             // A/B probes: 1 skip the compare loop, 2 no norm loads
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -63,7 +65,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
@@ -220,43 +222,75 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int64_t self_col = (A.self_off >= 0 && live) ? row + A.self_off : -1;
         float* lv = reinterpret_cast<float*>(sm + A.o_lv);    // [kc][BM], column per thread
         int32_t* li = reinterpret_cast<int32_t*>(sm + A.o_li);
+        float* nb = reinterpret_cast<float*>(sm + A.o_nb);    // [2][BN] column norms per accumulator
+        float* scr = reinterpret_cast<float*>(sm + A.o_scr);  // [32][BM] slow-path values
         const int KC = A.kc;
         for (int k = 0; k < KC; k++) {
             lv[k * BM + r_local] = __int_as_float(0x7f800000);
             li[k * BM + r_local] = -1;
         }
-        float tau = __int_as_float(0x7f800000);  // the list's current worst
+        const float inf = __int_as_float(0x7f800000);
+        float tau = inf;  // the list's current worst
         int tpos = 0;
+        // column norms one tile ahead (thread i < BN loads norm i, coalesced);
+        // columns past n get +inf, so zero-filled rows never qualify
+        auto norm_of = [&](int64_t t) -> float {
+            const int64_t c = t * BN + r_local;
+            return (r_local < BN && c < A.n && !(A.debug & 2)) ? __ldg(A.xn + c) : (c < A.n ? 0.f : inf);
+        };
+        float nnext = norm_of(0);
         for (int64_t t = 0; t < ntiles; t++) {
             const int buf = (int)(t & 1);
             const uint32_t aph = (uint32_t)((t >> 1) & 1);
+            if (r_local < BN) nb[buf * BN + r_local] = nnext;
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the 4 epilogue warps
+            nnext = t + 1 < ntiles ? norm_of(t + 1) : 0.f;
             mbar_wait(acc_full + buf, aph);
             tc_fence_after();
             const int64_t c_base = t * BN;
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            const float4* nb4 = reinterpret_cast<const float4*>(nb + buf * BN);
+            for (int c0 = 0; c0 < BN && !(A.debug & 1); c0 += 32) {
                 float acc[32];
                 tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + c0), acc);
-                const int64_t cb = c_base + c0;
-                const bool full32 = cb + 32 <= A.n;
+                // fast path: 32 values, four independent running minima
+                float m0 = inf, m1 = inf, m2 = inf, m3 = inf;
 #pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    const int64_t col = cb + i;
-                    const bool in = full32 || col < A.n;
-                    const float v = __fmaf_rn(-2.f, acc[i], in ? __ldg(A.xn + col) : 0.f);
-                    if (in && v < tau && col != self_col) {
-                        lv[tpos * BM + r_local] = v;
-                        li[tpos * BM + r_local] = (int32_t)col;
-                        float w = lv[r_local];
-                        int wp = 0;
-                        for (int k = 1; k < KC; k++) {
-                            const float x = lv[k * BM + r_local];
-                            if (x > w) {
-                                w = x;
-                                wp = k;
+                for (int i = 0; i < 32; i += 4) {
+                    const float4 xn4 = nb4[(c0 + i) >> 2];
+                    acc[i] = __fmaf_rn(-2.f, acc[i], xn4.x);
+                    acc[i + 1] = __fmaf_rn(-2.f, acc[i + 1], xn4.y);
+                    acc[i + 2] = __fmaf_rn(-2.f, acc[i + 2], xn4.z);
+                    acc[i + 3] = __fmaf_rn(-2.f, acc[i + 3], xn4.w);
+                    m0 = fminf(m0, acc[i]);
+                    m1 = fminf(m1, acc[i + 1]);
+                    m2 = fminf(m2, acc[i + 2]);
+                    m3 = fminf(m3, acc[i + 3]);
+                }
+                if (fminf(fminf(m0, m1), fminf(m2, m3)) < tau) {
+                    // slow path (rare once the list is warm): park the 32
+                    // values in this thread's scratch column (registers stay
+                    // statically indexed), then insert
+                    const int64_t cb = c_base + c0;
+#pragma unroll
+                    for (int i = 0; i < 32; i++) scr[i * BM + r_local] = acc[i];
+#pragma unroll 1
+                    for (int i = 0; i < 32; i++) {
+                        const float v = scr[i * BM + r_local];
+                        if (v < tau && cb + i != self_col) {
+                            lv[tpos * BM + r_local] = v;
+                            li[tpos * BM + r_local] = (int32_t)(cb + i);
+                            float w = lv[r_local];
+                            int wp = 0;
+                            for (int k = 1; k < KC; k++) {
+                                const float x = lv[k * BM + r_local];
+                                if (x > w) {
+                                    w = x;
+                                    wp = k;
+                                }
                             }
+                            tau = w;
+                            tpos = wp;
                         }
-                        tau = w;
-                        tpos = wp;
                     }
                 }
             }
@@ -321,6 +355,7 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
                                   const float* xn, int64_t self_off, int32_t kc, int32_t* out_ids,
                                   float* out_vals, void* stream, char* msg) {
     using namespace knn;
+    static const int debug = getenv("PW_KNN_DEBUG") ? atoi(getenv("PW_KNN_DEBUG")) : 0;
     if (nq <= 0) return 0;
     if (!q || !x || !xn || !out_ids || !out_vals || n <= 0 || d < 1 || kc < 1 || kc > 64 || n >= (1ll << 31) ||
         nq >= (1ll << 31) || (d * 4) % 16 != 0) {
@@ -339,7 +374,7 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     int bn = 0, st = 0;
     for (int cand_bn : {128, 64, 32})
         for (int cand_st : {4, 3, 2}) {
-            const size_t need = a_bytes + (size_t)cand_st * cand_bn * ka * ATOM + 1024 + lists + 1024;
+            const size_t need = a_bytes + (size_t)cand_st * cand_bn * ka * ATOM + 1024 + lists + 2048 + 32 * BM * 4;
             if (!bn && need <= (size_t)optin) {
                 bn = cand_bn;
                 st = cand_st;
@@ -361,6 +396,7 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     A.xn = xn;
     A.out_ids = out_ids;
     A.out_vals = out_vals;
+    A.debug = debug;
     size_t off = a_bytes;
     A.o_b = (uint32_t)off;
     off += (size_t)st * bn * ka * ATOM;
@@ -373,6 +409,10 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     off += (size_t)kc * BM * 4;
     A.o_li = (uint32_t)off;
     off += (size_t)kc * BM * 4;
+    A.o_nb = (uint32_t)off;
+    off += (size_t)2 * bn * 4;
+    A.o_scr = (uint32_t)off;
+    off += (size_t)32 * BM * 4;
     CUtensorMap tq, tx;
     if (!knn_map(&tq, q, nq, d, BM) || !knn_map(&tx, x, n, d, bn)) {
         snprintf(msg, 256, "knn screen: cuTensorMapEncodeTiled failed");

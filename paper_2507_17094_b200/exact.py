@@ -226,15 +226,23 @@ def _reverse_augment(x: torch.Tensor, adj: torch.Tensor) -> torch.Tensor:
     return out.to(torch.int32)
 
 
-def build_knn_graph(x: torch.Tensor, j: int) -> torch.Tensor:
+def build_knn_graph(x: torch.Tensor, j: int, stats: dict | None = None) -> torch.Tensor:
     """graphs.py:104-134 exact j-NN graph + reverse augmentation, (n, j) int32."""
     n = x.shape[0]
     if not 0 <= j < n:
         raise ValueError(f"need 0 <= j < n_local, got j={j}, n_local={n}")
     if j == 0:
         return torch.empty((n, 0), dtype=torch.int32, device=x.device)
-    adj, _ = exact_topk(x, x, j, exclude_self=True)
-    return _reverse_augment(x, adj)
+    t0 = time.perf_counter()
+    adj, _ = exact_topk(x, x, j, exclude_self=True, stats=stats)
+    if stats is not None:
+        torch.cuda.synchronize(x.device)
+        t1 = time.perf_counter()
+    out = _reverse_augment(x, adj)
+    if stats is not None:
+        torch.cuda.synchronize(x.device)
+        stats.update(knn_s=round(t1 - t0, 2), augment_s=round(time.perf_counter() - t1, 2))
+    return out
 
 
 def build_inter_shard_table(src: torch.Tensor, dst: torch.Tensor) -> torch.Tensor:

@@ -20,6 +20,18 @@ FIXTURES = {  # make_golden.py build_index arguments
 
 @pytest.mark.parametrize("name", sorted(FIXTURES))
 def test_build_index_matches_reference(name):
+    _check_build(name)
+
+
+@pytest.mark.parametrize("name", sorted(FIXTURES))
+def test_build_index_tensor_core_screen_matches_reference(name, monkeypatch):
+    """Every screen through K4 (tcgen05 TF32 + certification + FP32 redo of
+    uncertified rows): the reference's indexes all the same."""
+    monkeypatch.setattr(exact, "TC_MIN_PAIRS", 0)
+    _check_build(name)
+
+
+def _check_build(name):
     z = np.load(GOLDEN / f"{name}.npz")
     kw = FIXTURES[name]
     index, report = exact.build_index(z["base"], kw["n_shards"], kw["j"], kw["seed"], rho=kw["rho"],
@@ -75,3 +87,27 @@ def test_build_errors():
 
     with pytest.raises(ValueError, match="too small for out-degree"):
         exact.build_ghost_index(torch.from_numpy(x).cuda(), 0.1, 8, 1)
+
+
+@pytest.mark.parametrize("d,n,nq,self_ex,dup", [(96, 40000, 3000, True, False), (128, 20000, 2000, False, False),
+                                                (200, 12000, 1000, True, False), (96, 30000, 2000, True, True),
+                                                (16, 40, 40, True, False)])
+def test_tensor_core_screen_topk_equals_fp32_screen(d, n, nq, self_ex, dup):
+    """exact_topk through K4 (certified, redo of the rest) == through the FP32
+    screen, ids and bit-exact distances; with duplicate rows (exact distance
+    ties, broken by id) and with fewer base rows than candidates."""
+    import torch
+
+    from paper_2507_17094_b200 import builder
+
+    x = builder.gen_latent(n, d, 16, 1, 1.0, 0.05, d + n, device="cuda")
+    if dup:
+        x[1::3] = x[0::3][: x[1::3].shape[0]]  # every third row duplicated
+    q = x[:nq].contiguous() if self_ex else builder.gen_latent(nq, d, 16, 1, 1.0, 0.05, 99, device="cuda")
+    k = min(32, n - 1)
+    st = {}
+    a_ids, a_sq = exact.exact_topk(x, q, k, exclude_self=self_ex, screen="tc", stats=st)
+    b_ids, b_sq = exact.exact_topk(x, q, k, exclude_self=self_ex, screen="fp32")
+    assert torch.equal(a_ids, b_ids), st
+    assert torch.equal(a_sq, b_sq)
+    assert st["certified"] + st["redone"] == nq
