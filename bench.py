@@ -5,8 +5,9 @@
 Workload (BASELINE.json configs[1], "C2"): DEEP-shaped 10M x 96 float32 base,
 10K queries, k=10, degree-32 graph, single B200 (multi-GPU: one shard per GPU,
 launched by torchrun).  Data are synthetic (gen_synthetic's clustered-Gaussian
-family on the GPU, fixed seed) and the index is built on the GPU by
-paper_2507_17094_b200.builder (setup, not timed).  A "step" is one full search
+family on the GPU, fixed seed) and the index is built on the GPU with the
+reference's exact-graph semantics (paper_2507_17094_b200.exact, K4 tensor-core
+screen + bit-exact rescore; setup, not timed).  A "step" is one full search
 of all 10K queries (ghost stage + pipelined path extension + direction-guided
 selection) followed by the top-k reduction; the operating point is the
 smallest queue length l whose recall@10 >= 0.95 (recall is measured against
@@ -41,18 +42,25 @@ CONFIGS = {
     # gen "latent": z ~ N(0, I_m) (m = intrinsic dim) lifted to d by a fixed random
     # linear map + isotropic noise (builder.gen_latent); "gauss": the reference's
     # gen_synthetic family (uniform centres + spread * N(0, I)).
+    # the reference's exact graph semantics (graphs.py:104-134: exact kNN +
+    # reverse augmentation, exact inter-shard and ghost graphs), built with
+    # the K4 tensor-core screen + certified bit-exact rescore (~80 s at 10M)
     "c2": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph",
                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
-               spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
+               spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, builder="exact"),
+    # round-1 C2: approximate IVF graph (keeps 85% of each row's exact 32-NN)
+    "c2ivf": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (IVF approximate graph)",
+                  n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
+                  spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
     # C2 on harder data: intrinsic dimension 64 instead of 16 (same shape)
     "c2h": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (latent dim 64)",
                 n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=64, n_clusters=1,
-                spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
+                spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, builder="exact"),
     # C2 on the reference's own generator family (gen_synthetic: uniform
     # centres + spread * N(0, I)), 10M rows in 100K clusters
     "c2g": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (gen_synthetic family)",
                 n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="gauss", n_clusters=100_000,
-                spread=0.08, rho=0.01, j_g=16, probe=192, refine=1),
+                spread=0.08, rho=0.01, j_g=16, probe=192, builder="exact"),
     "c1": dict(workload="SIFT-shaped 100K x 128 f32, 1K queries, k=10, degree-32 graph",
                n=100_000, d=128, nq=1_000, k=10, j=32, gen="gauss", n_clusters=8192,
                spread=0.08, rho=0.01, j_g=16, probe=32, builder="exact"),
@@ -64,7 +72,7 @@ CONFIGS = {
     "c3s": dict(workload="SIFT-shaped 12.5M x 128 uint8 (one of C3's 8 shards of 100M), 10K queries, "
                          "k=10, degree-32 graph", n=12_500_000, d=128, nq=10_000, k=10, j=32,
                 gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192,
-                refine=1, dtype="u8"),
+                builder="exact", dtype="u8"),
     "c4": dict(workload="GIST-shaped 1M x 960 f32, 1K queries, k=10, degree-32 graph", n=1_000_000,
                d=960, nq=1_000, k=10, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05,
                rho=0.01, j_g=16, probe=48, builder="exact"),
@@ -586,6 +594,7 @@ def traffic_for(cfg: dict, l: int, discard: float = 0.5, ghost_iter: int = 8):
             if t.get("workload") == cfg["workload"] and t.get("l") == l and \
                     float(t.get("dgs_discard", 0.5)) == float(discard) and \
                     int(t.get("ghost_max_iter", 8)) == int(ghost_iter) and \
+                    t.get("builder", "ivf") == cfg.get("builder", "ivf") and \
                     (cfg.get("builder") == "exact" or (int(t.get("probe", 48)) == int(probe) and
                                                        int(t.get("refine", 0)) == int(cfg.get("refine", 0)))):
                 return int(t["traffic_bytes_per_launch"])

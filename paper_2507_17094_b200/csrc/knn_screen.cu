@@ -111,9 +111,10 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// 32 consecutive fp32 columns of this thread's TMEM lane
-__device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
-    uint32_t r[32];
+// 32 consecutive fp32 columns of this thread's TMEM lane; the caller waits
+// (tcgen05.wait::ld) before touching v, so a load can overlap other work
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t addr, float (&v)[32]) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(v);
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
         "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
@@ -122,10 +123,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
           "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
     knn_screen_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_x,
@@ -249,9 +248,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tc_fence_after();
             const int64_t c_base = t * BN;
             const float4* nb4 = reinterpret_cast<const float4*>(nb + buf * BN);
-            for (int c0 = 0; c0 < BN && !(A.debug & 1); c0 += 32) {
-                float acc[32];
-                tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + c0), acc);
+            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN);
+            float accb[2][32];
+            tmem_ld32_issue(taddr, accb[0]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                if (c0 >= BN || (A.debug & 1)) break;
+                float (&acc)[32] = accb[(c0 >> 5) & 1];
+                // the next chunk's TMEM load overlaps this chunk's compare
+                if (c0 + 32 < BN) tmem_ld32_issue(taddr + (uint32_t)(c0 + 32), accb[((c0 >> 5) + 1) & 1]);
                 // fast path: 32 values, four independent running minima
                 float m0 = inf, m1 = inf, m2 = inf, m3 = inf;
 #pragma unroll
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                         }
                     }
                 }
+                tmem_ld_wait();
             }
             tc_fence_before();
             __syncwarp();
