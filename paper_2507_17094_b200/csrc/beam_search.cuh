@@ -113,6 +113,7 @@ struct KArgs {
     int32_t L_max, CB, BH, H, R, PG;
     int32_t pstride;        // DGS parent-row stride in elements (16-byte multiple)
     int32_t o_par;          // parents list offset in misc (words)
+    int32_t o_qbits;        // DGS query-bit words (PW_DGS_LDG) offset in misc (words)
     int32_t o_q, o_qk, o_qe, o_cand, o_cslot, o_newl, o_ckey, o_bhk, o_bhp, o_vh, o_stage,
         o_misc, o_mbar, o_desc, warp_bytes;
     int32_t bulk_rows;      // vector rows may use cp.async.bulk (TMA) (d*4 % 16 == 0)
@@ -284,6 +285,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // path is slower than LDGSTS (PW 1.62 vs 1.52 ms, naive 3.22 vs 2.88 ms) and
 // merely compiling it in costs 3-5% (code size / registers in the hot loop);
 // build with -DPW_TMA_ROWS=1 for the A/B (tests pass either way).
+#ifndef PW_DGS_LDG
+#define PW_DGS_LDG 0  // DGS parent rows into registers instead of the staging ring (A/B)
+#endif
 #ifndef PW_TMA_ROWS
 #define PW_TMA_ROWS 0
 #endif
@@ -1369,7 +1373,7 @@ static __device__ __noinline__ uint32_t bulk_issue_wait(const uint4* desc, uint6
 // LDGSTS chunks.  TMA bulk copies need warp-uniform operands, so per-row
 // (data-dependent) sources make ptxas serialise lanes through a waterfall
 // loop of hundreds of instructions; this is a dozen.
-static __device__ __forceinline__ void copy16_issue_wait(const uint4* desc, int n_rows) {
+static __device__ __forceinline__ void copy16_issue_wait(const uint4* desc, int n_rows, bool wait = true) {
     const unsigned lane = lane_id();
     const unsigned sub = lane & 7u;
     const uint64_t pol = l2_evict_first_policy();
@@ -1380,6 +1384,7 @@ static __device__ __forceinline__ void copy16_issue_wait(const uint4* desc, int 
         for (uint32_t c = sub; c < nch; c += 8) cp_async16_stream(d.x + 16 * c, src + 16 * c, pol);
     }
     cp_commit();
+    if (!wait) return;
     cp_wait<0>();
     __syncwarp();
 }
@@ -1413,7 +1418,7 @@ static __device__ __noinline__ void copy_issue_wait(const uint4* desc, int n_row
 // out-of-line issuer runs TMA bulk copies (aligned rows) or cp.async.
 template <typename F>
 __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_rows, uint32_t total,
-                                            F&& row) {
+                                            F&& row, bool wait = true) {
     const unsigned lane = lane_id();
     for (int r = lane; r < n_rows; r += 32) {
         void* dst;
@@ -1427,7 +1432,7 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
     if (A.bulk_adj == 2)
         S.phase = bulk_issue_wait(S.desc, S.mbar + 2, S.phase, n_rows, total);
     else if (A.bulk_adj)
-        copy16_issue_wait(S.desc, n_rows);
+        copy16_issue_wait(S.desc, n_rows, wait);
     else
         copy_issue_wait(S.desc, n_rows);
 }
@@ -1489,10 +1494,65 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
         const int W = WC ? WC : A.W;
         const int d = D > 0 ? D : A.d;
         const uint32_t vec_bytes = (uint32_t)d * (uint32_t)sizeof(VT), dir_bytes = (uint32_t)(j * W) * 4u;
+        // PW_DGS_LDG: the parents' query bits pack(q >= x_parent) from their
+        // rows loaded straight into registers (one float4 per lane and parent,
+        // in flight with the expansion's cp.async round trip), so the parent
+        // rows never pass through the staging ring
+        constexpr bool LDGP = PW_DGS_LDG && D > 0 && sizeof(VT) == 4 && D % 4 == 0 && D <= 128;
+        [[maybe_unused]] uint32_t* qbits = reinterpret_cast<uint32_t*>(S.misc + A.o_qbits);
         for (int pg = 0; pg < np; pg += A.PG) {
             const int gp = min(A.PG, np - pg);
             VT* prow = reinterpret_cast<VT*>(S.stage);
-            uint32_t* drow = reinterpret_cast<uint32_t*>(prow + (size_t)gp * A.pstride);
+            uint32_t* drow = LDGP ? reinterpret_cast<uint32_t*>(S.stage)
+                                  : reinterpret_cast<uint32_t*>(prow + (size_t)gp * A.pstride);
+            if constexpr (LDGP) {
+                constexpr int CH = D / 4;  // float4 chunks per row
+                // cp.async of the adjacency + direction rows issued first
+                // (no wait), then the parent rows' register loads: one round trip
+                fetch_group(A, S, 2 * gp, gp * (adj_bytes + dir_bytes),
+                            [&](int r, void*& dst, const void*& src, uint32_t& b) {
+                                const int pi = r % gp;
+                                const int32_t par = parents[pg + pi];
+                                if (r < gp) {
+                                    dst = craw + (pg + pi) * j;
+                                    src = G.adj + (size_t)par * j;
+                                    b = adj_bytes;
+                                } else {
+                                    dst = drow + (size_t)pi * j * W;
+                                    src = G.dir + (size_t)par * j * W;
+                                    b = dir_bytes;
+                                }
+                            }, /*wait=*/!A.bulk_adj || A.bulk_adj == 2);
+                float4 xr[kParentGroup];
+#pragma unroll
+                for (int pi = 0; pi < kParentGroup; pi++)
+                    if (pi < gp && (int)lane < CH)
+                        xr[pi] = __ldcs(reinterpret_cast<const float4*>(vrow<VT>(G, (uint32_t)parents[pg + pi], D)) +
+                                        lane);
+                if (A.bulk_adj == 1) {
+                    cp_wait<0>();
+                    __syncwarp();
+                }
+                const float4 q4 = (int)lane < CH ? reinterpret_cast<const float4*>(S.q)[lane]
+                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int pi = 0; pi < kParentGroup; pi++) {
+                    if (pi < gp) {
+                        // lane holds elements 4 lane .. 4 lane + 3: a nibble of
+                        // word lane / 8, OR-reduced over the 8 lanes of a word
+                        const float4 x = xr[pi];
+                        uint32_t v = (int)lane < CH ? ((q4.x >= x.x ? 1u : 0u) | (q4.y >= x.y ? 2u : 0u) |
+                                                       (q4.z >= x.z ? 4u : 0u) | (q4.w >= x.w ? 8u : 0u))
+                                                    : 0u;
+                        v <<= 4u * (lane & 7u);
+                        v |= __shfl_xor_sync(0xffffffffu, v, 1);
+                        v |= __shfl_xor_sync(0xffffffffu, v, 2);
+                        v |= __shfl_xor_sync(0xffffffffu, v, 4);
+                        if ((lane & 7u) == 0 && (int)(lane >> 3) < WC) qbits[pi * WC + (lane >> 3)] = v;
+                    }
+                }
+                __syncwarp();
+            } else
             fetch_group(A, S, 3 * gp, gp * (adj_bytes + vec_bytes + dir_bytes),
                         [&](int r, void*& dst, const void*& src, uint32_t& b) {
                             const int pi = r % gp, kind = r / gp;
@@ -1521,9 +1581,13 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                     uint32_t qb[WC > 0 ? WC : 1];
 #pragma unroll
                     for (int w = 0; w < WC; w++) {
-                        const int t = 32 * w + (int)lane;
-                        const bool bit = t < d && S.q[t] >= to_f(prow[(size_t)pi * A.pstride + t]);
-                        qb[w] = __ballot_sync(0xffffffffu, bit);
+                        if constexpr (LDGP) {
+                            qb[w] = qbits[pi * WC + w];
+                        } else {
+                            const int t = 32 * w + (int)lane;
+                            const bool bit = t < d && S.q[t] >= to_f(prow[(size_t)pi * A.pstride + t]);
+                            qb[w] = __ballot_sync(0xffffffffu, bit);
+                        }
                     }
                     int c = 0;
                     if ((int)lane < j) {

@@ -631,8 +631,12 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // bank-conflict concern) so that kParentGroup parents fit the staging
     // ring and one expansion is ONE fetch round trip (C2: 8 x (96 + 96) words)
     const int pstride = elem == 4 ? (d + 3) & ~3 : (d + 15) & ~15;  // elements, 16-byte rows
+    // PW_DGS_LDG (specialised f32 kernels, d <= 128): parent rows go to
+    // registers, only adjacency + direction rows to the staging ring
+    const bool dgs_ldg = PW_DGS_LDG && specialised && elem == 4 && d % 4 == 0 && d <= 128 && G.j <= 32;
+    const int64_t per_vec = dgs_ldg ? 0 : (int64_t)pstride * elem;
     if (A.cfg.prune_sel == PW_SEL_DIRECTION) {
-        const int64_t per = (int64_t)pstride * elem + 4ll * G.j * W;  // bytes per parent
+        const int64_t per = per_vec + 4ll * G.j * W;  // bytes per parent
         while ((int64_t)R * spad * elem < per) R += 2;
         PG = (int)std::min<int64_t>(kParentGroup, ((int64_t)R * spad * elem) / per);
         PG = std::max(PG, 1);
@@ -650,7 +654,7 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         const int64_t hash_bytes = 8 * (int64_t)A.BH + 4 * cb;
         const int64_t stage_bytes = std::max<int64_t>((int64_t)elem * Rr * spad, hash_bytes);
         if (A.cfg.prune_sel == PW_SEL_DIRECTION) {  // DGS parents per fetch round trip
-            const int64_t per = (int64_t)pstride * elem + 4ll * G.j * W;
+            const int64_t per = per_vec + 4ll * G.j * W;
             PG = (int)std::max<int64_t>(1, std::min<int64_t>(kParentGroup, stage_bytes / per));
         }
         A.PG = PG;
@@ -682,7 +686,8 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         // misc words: [DGS counts PG*j | perm j] [DGS bits PG*W] 8 pad (task
         // scalars) | parents r | 8 pad
         const int64_t misc_cnt = dgs_regs ? (int64_t)jm : (int64_t)std::max(jm, PG * jm);
-        const int64_t misc_bits = dgs_regs ? 0 : (int64_t)PG * W;
+        const int64_t misc_bits = (dgs_regs && !dgs_ldg) ? 0 : (int64_t)PG * W;
+        A.o_qbits = (int32_t)misc_cnt;
         A.o_par = (int32_t)(misc_cnt + misc_bits + 8);
         const int64_t misc = misc_cnt + misc_bits + 8 + p.r + 8;
         off = al(off + 4 * misc);

@@ -86,8 +86,16 @@ for N in (int(x) for x in args.ns.split(",")):
         rec = recall(p, "baseline")
         if rec >= 0.95:
             break
+    def work(stats):
+        """mean per query, summed over stages: distance computations, iterations"""
+        return {"dc_per_query": round(float(sum(s["distance_computations"].sum() for s in stats)) / q.shape[0], 1),
+                "iterations_per_query": round(float(sum(s["iterations"].sum() + s["ghost_iterations"].sum()
+                                                        for s in stats)) / q.shape[0], 2)}
+
     out["naive"] = {"l": l, "recall": round(rec, 4),
                     "ms": round(timed(lambda: dv.run_local(shards, p, q, "baseline", run, tuning=tuning)), 3)}
+    dv.run_local(shards, p, q, "baseline", run)  # exact visited set: reference-exact counters
+    out["naive"].update(work(run.stats()))
     best = None
     for how in ("pipelined", "dataflow"):
         grid = [tuple(float(v) for v in x.split(":")) for x in args.pw_grid.split(",")] if args.pw_grid \
@@ -111,6 +119,11 @@ for N in (int(x) for x in args.ns.split(",")):
                 best = cand
     out["pathweaver"] = best
     out["pw_over_naive"] = round(out["naive"]["ms"] / best["ms"], 3) if best else None
+    if best:
+        pb = bench.arm_params("pathweaver", best["l"], k, discard=best["discard"], ghost_iter=best["ghost_max_iter"])
+        dv.run_local(shards, pb, q, "pipelined", run)
+        best.update(work(run.stats()))
+        out["dc_ratio_naive_over_pw"] = round(out["naive"]["dc_per_query"] / best["dc_per_query"], 3)
     if args.ext and best:
         # opt-in knobs beyond the reference (results differ from it): forward
         # the top-F entries, smaller queue / iteration budget
