@@ -52,15 +52,20 @@ CONFIGS = {
     "c2ivf": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (IVF approximate graph)",
                   n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=16, n_clusters=1,
                   spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, refine=1),
-    # C2 on harder data: intrinsic dimension 64 instead of 16 (same shape)
-    "c2h": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (latent dim 64)",
-                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=64, n_clusters=1,
+    # C2 on harder data: intrinsic dimension 32 instead of 16 (same shape; at
+    # 64 neither arm reaches recall 0.95 by l = 512: 0.73 / 0.77,
+    # profiles/r02/bench_c2h_m64_r02u.json)
+    "c2h": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (latent dim 32)",
+                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="latent", m=32, n_clusters=1,
                 spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=192, builder="exact"),
     # C2 on the reference's own generator family (gen_synthetic: uniform
-    # centres + spread * N(0, I)), 10M rows in 100K clusters
+    # centres + spread * N(0, I)) with its defaults (64 clusters, spread 0.2);
+    # with 100K clusters of 100 rows the exact kNN graph falls apart into one
+    # component per cluster and neither arm finds the query's cluster
+    # (recall 0.0007 / 0.0005, profiles/r02/bench_c2g_100kclusters_r02u.json)
     "c2g": dict(workload="DEEP-shaped 10M x 96 f32, 10K queries, k=10, degree-32 graph (gen_synthetic family)",
-                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="gauss", n_clusters=100_000,
-                spread=0.08, rho=0.01, j_g=16, probe=192, builder="exact"),
+                n=10_000_000, d=96, nq=10_000, k=10, j=32, gen="gauss", n_clusters=64,
+                spread=0.2, rho=0.01, j_g=16, probe=192, builder="exact"),
     "c1": dict(workload="SIFT-shaped 100K x 128 f32, 1K queries, k=10, degree-32 graph",
                n=100_000, d=128, nq=1_000, k=10, j=32, gen="gauss", n_clusters=8192,
                spread=0.08, rho=0.01, j_g=16, probe=32, builder="exact"),
