@@ -206,6 +206,14 @@ int pw_search_dataflow(pw_shard* shard, const pw_params* params, const pw_tuning
 int pw_l2_pairs(const float* a, const float* b, int32_t d, const int64_t* ia, const int64_t* ib,
                 int64_t n, float* out, void* stream);
 
+/* Measurement probe (not a reference interface): gather n_ids rows of
+ * row_bytes (a 16-byte multiple) from table at random ids with as many rows
+ * in flight as the SMs hold -- the achievable HBM bandwidth of K1's access
+ * pattern, reported beside K1's roofline (tools/gather_probe.py).  Device
+ * pointers; sink: one device u32; asynchronous. */
+int pw_gather_probe(const void* table, int64_t row_bytes, const int32_t* ids, int64_t n_ids,
+                    uint32_t* sink, int32_t blocks, void* stream);
+
 /* K4 tensor-core kNN screen (replaces the distance screen of
  * graphs.py:65-78 `_knn_block`, which keeps k + 8 candidates per row by a
  * GEMM-style distance before the exact rescore): for each of the nq query

@@ -75,7 +75,9 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
                  ([nv, *CFLAGS, *extra, "-c", str(CSRC / "pw_crc32c.cu"), "-o", str(bdir / "pw_crc32c.o")],
                   bdir / "pw_crc32c.o"),
                  ([nv, *CFLAGS, *extra, "-c", str(CSRC / "knn_screen.cu"), "-o", str(bdir / "knn_screen.o")],
-                  bdir / "knn_screen.o")]
+                  bdir / "knn_screen.o"),
+                 ([nv, *CFLAGS, *extra, "-c", str(CSRC / "gather_probe.cu"), "-o", str(bdir / "gather_probe.o")],
+                  bdir / "gather_probe.o")]
     for d in DIMS:
         obj = bdir / f"k_{d}.o"
         jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",
