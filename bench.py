@@ -94,7 +94,7 @@ CONFIGS = {
 # probe 48 42%, 192 69%, 192 + one refinement pass 85% (setup 29 -> 72 s);
 # both arms' operating points fall with it (naive l 256 -> 144 -> 128, PW l
 # 256 -> 160 -> 144; K1 naive 4.84 -> 3.39 -> 3.06, PW 2.77 -> 1.98 -> 1.85 ms).
-L_GRID = (32, 48, 64, 80, 96, 112, 128, 144, 160, 176, 192, 224, 256, 288, 320, 384, 512)
+L_GRID = (32, 48, 64, 80, 96, 112, 128, 144, 160, 176, 192, 224, 256, 288, 320, 384, 512, 640, 768, 1024)
 # lossy visited cache (K1 tuning flag 2): same ids/distances/counters as the
 # exact set except distance_computations; both arms use it
 DEFAULT_TUNING = '{"flags": 2}'
