@@ -220,12 +220,10 @@ int pw_gather_probe(const void* table, int64_t row_bytes, const int32_t* ids, in
  * rows q (device, (nq, d) f32), the kc base rows x (device, (n, d) f32) with
  * the smallest approximate |x_c|^2 - 2 q.x_c (TF32 tensor cores, FP32
  * accumulation; xn = |x_c|^2, (n,) f32), query row r excluding base row
- * r + self_off when self_off >= 0.  Outputs (nq, kc) int32 ids / f32 values
- * as two unsorted half-lists: columns [0, kc/2) hold the kc/2 smallest of the
- * first half of every column tile, [kc/2, kc) those of the second half (-1 /
- * +inf where a half has fewer columns).  d % 4 == 0, even kc <= 64.  The
- * values only select candidates: exact.py rescores them bit-exactly and
- * certifies each row against the TF32 error bound. */
+ * r + self_off when self_off >= 0.  Outputs (nq, kc) int32 ids / f32 values,
+ * unsorted, -1 / +inf when n - 1 < kc.  d % 4 == 0, kc <= 64.  The values only
+ * select candidates: exact.py rescores them bit-exactly and certifies each
+ * row against the TF32 error bound. */
 int pw_knn_screen(const float* q, int64_t nq, const float* x, int64_t n, int32_t d, const float* xn,
                   int64_t self_off, int32_t kc, int32_t* out_ids, float* out_vals, void* stream);
 

@@ -8,12 +8,11 @@
 //   warp 1      MMA issuer: tcgen05.mma kind::tf32 (M=128, N=BN, K=8 per
 //               instruction) into one of two TMEM accumulators (BN columns
 //               each), tcgen05.commit to free ring slots / hand a tile over
-//   warps 2..9  epilogue, two per TMEM lane quadrant: tcgen05.ld of the row's
-//               accumulators for one half of the tile's columns, approximate
-//               squared distance |x_c|^2 - 2 q.x_c, and per (row, column half)
-//               a list of the KC/2 smallest (self excluded) in shared memory;
-//               a value only enters when it beats that list's current worst
-//               (a compare per value once the list is warm)
+//   warps 2..5  epilogue: tcgen05.ld of the row's BN accumulators, approximate
+//               squared distance |x_c|^2 - 2 q.x_c, and a per-row list of the
+//               KC smallest (self excluded) in shared memory; a value only
+//               enters when it beats the row's current worst (a compare per
+//               value once the list is warm)
 // Nothing of the n x n distance matrix is ever written to memory.  The
 // approximate values (TF32 operands, FP32 accumulation) only SELECT
 // candidates: the builder rescores them with the bit-exact numpy-pairwise L2
@@ -29,8 +28,7 @@
 namespace knn {
 
 constexpr int BM = 128;        // query rows per CTA (MMA M, TMEM lanes)
-constexpr int EPI_WARPS = 8;    // two per TMEM lane quadrant, one per column half
-constexpr int NTHREADS = 64 + 32 * EPI_WARPS;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int NTHREADS = 192;  // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
 constexpr int ATOM = 128;      // bytes per 128B-swizzle row (32 fp32 of K)
 
 struct Args {
@@ -41,7 +39,7 @@ struct Args {
     const float* xn;           // (n,) |x_c|^2
     int32_t* out_ids;          // (nq, kc)
     float* out_vals;           // (nq, kc)
-    uint32_t o_b, o_bar, o_lv, o_li, o_tmem, o_nb;  // shared-memory offsets
+    uint32_t o_b, o_bar, o_lv, o_li, o_tmem, o_nb, o_scr;  // shared-memory offsets
     int32_t debug;             // A/B probes: 1 skip the compare loop, 2 no norm loads
 };
 
@@ -155,7 +153,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(acc_full + b, 1);
-            mbar_init(acc_empty + b, EPI_WARPS);  // one arrive per epilogue warp
+            mbar_init(acc_empty + b, 4);  // one arrive per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -216,57 +214,50 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
     } else {
         // ---------------- epilogue: warp w reads TMEM lanes 32 * (w % 4) ..
-        // and one half of each tile's columns; each (row, half) keeps its own
-        // list of the KC/2 smallest, so no state is shared between warps.  A
-        // column outside the union of a row's two lists is >= the smaller
-        // of the two lists' worst values (exact.py certifies with that).
         const int quad = warp & 3;
-        const int half = (warp - 2) >> 2;
         const int r_local = quad * 32 + lane;
         const int64_t row = row0 + r_local;
         const bool live = row < A.nq;
         const int64_t self_col = (A.self_off >= 0 && live) ? row + A.self_off : -1;
-        const int KH = A.kc / 2;  // entries per half-list
-        float* lv = reinterpret_cast<float*>(sm + A.o_lv) + (size_t)half * KH * BM;    // [KH][BM]
-        int32_t* li = reinterpret_cast<int32_t*>(sm + A.o_li) + (size_t)half * KH * BM;
+        float* lv = reinterpret_cast<float*>(sm + A.o_lv);    // [kc][BM], column per thread
+        int32_t* li = reinterpret_cast<int32_t*>(sm + A.o_li);
         float* nb = reinterpret_cast<float*>(sm + A.o_nb);    // [2][BN] column norms per accumulator
-        const int HB = BN / 2;                                // columns per half
-        const int c_lo = half * HB;
-        for (int k = 0; k < KH; k++) {
+        float* scr = reinterpret_cast<float*>(sm + A.o_scr);  // [32][BM] slow-path values
+        const int KC = A.kc;
+        for (int k = 0; k < KC; k++) {
             lv[k * BM + r_local] = __int_as_float(0x7f800000);
             li[k * BM + r_local] = -1;
         }
         const float inf = __int_as_float(0x7f800000);
-        float tau = inf;  // this half-list's current worst
+        float tau = inf;  // the list's current worst
         int tpos = 0;
-        const int et = (warp - 2) * 32 + lane;  // 0 .. 255 over the epilogue warps
-        // column norms one tile ahead (thread et < BN loads norm et, coalesced);
+        // column norms one tile ahead (thread i < BN loads norm i, coalesced);
         // columns past n get +inf, so zero-filled rows never qualify
         auto norm_of = [&](int64_t t) -> float {
-            const int64_t c = t * BN + et;
-            return (et < BN && c < A.n && !(A.debug & 2)) ? __ldg(A.xn + c) : (c < A.n ? 0.f : inf);
+            const int64_t c = t * BN + r_local;
+            return (r_local < BN && c < A.n && !(A.debug & 2)) ? __ldg(A.xn + c) : (c < A.n ? 0.f : inf);
         };
         float nnext = norm_of(0);
         for (int64_t t = 0; t < ntiles; t++) {
             const int buf = (int)(t & 1);
             const uint32_t aph = (uint32_t)((t >> 1) & 1);
-            if (et < BN) nb[buf * BN + et] = nnext;
-            asm volatile("bar.sync 1, %0;\n" ::"n"(32 * EPI_WARPS) : "memory");  // the epilogue warps
+            if (r_local < BN) nb[buf * BN + r_local] = nnext;
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the 4 epilogue warps
             nnext = t + 1 < ntiles ? norm_of(t + 1) : 0.f;
             mbar_wait(acc_full + buf, aph);
             tc_fence_after();
-            const int64_t c_base = t * BN + c_lo;
-            const float4* nb4 = reinterpret_cast<const float4*>(nb + buf * BN + c_lo);
-            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + c_lo);
+            const int64_t c_base = t * BN;
+            const float4* nb4 = reinterpret_cast<const float4*>(nb + buf * BN);
+            const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN);
             float accb[2][32];
             tmem_ld32_issue(taddr, accb[0]);
             tmem_ld_wait();
 #pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 32) {
-                if (c0 >= HB || (A.debug & 1)) break;
+            for (int c0 = 0; c0 < 128; c0 += 32) {
+                if (c0 >= BN || (A.debug & 1)) break;
                 float (&acc)[32] = accb[(c0 >> 5) & 1];
                 // the next chunk's TMEM load overlaps this chunk's compare
-                if (c0 + 32 < HB) tmem_ld32_issue(taddr + (uint32_t)(c0 + 32), accb[((c0 >> 5) + 1) & 1]);
+                if (c0 + 32 < BN) tmem_ld32_issue(taddr + (uint32_t)(c0 + 32), accb[((c0 >> 5) + 1) & 1]);
                 // fast path: 32 values, four independent running minima
                 float m0 = inf, m1 = inf, m2 = inf, m3 = inf;
 #pragma unroll
@@ -282,17 +273,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     m3 = fminf(m3, acc[i + 3]);
                 }
                 if (fminf(fminf(m0, m1), fminf(m2, m3)) < tau) {
-                    // slow path (rare once the list is warm), statically
-                    // indexed so the values stay in registers
+                    // slow path (rare once the list is warm): park the 32
+                    // values in this thread's scratch column (registers stay
+                    // statically indexed), then insert
                     const int64_t cb = c_base + c0;
 #pragma unroll
+                    for (int i = 0; i < 32; i++) scr[i * BM + r_local] = acc[i];
+#pragma unroll 1
                     for (int i = 0; i < 32; i++) {
-                        if (acc[i] < tau && cb + i != self_col) {
-                            lv[tpos * BM + r_local] = acc[i];
+                        const float v = scr[i * BM + r_local];
+                        if (v < tau && cb + i != self_col) {
+                            lv[tpos * BM + r_local] = v;
                             li[tpos * BM + r_local] = (int32_t)(cb + i);
                             float w = lv[r_local];
                             int wp = 0;
-                            for (int k = 1; k < KH; k++) {
+                            for (int k = 1; k < KC; k++) {
                                 const float x = lv[k * BM + r_local];
                                 if (x > w) {
                                     w = x;
@@ -311,9 +306,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (lane == 0) mbar_arrive(acc_empty + buf);
         }
         if (live) {
-            for (int k = 0; k < KH; k++) {
-                A.out_ids[row * A.kc + half * KH + k] = li[k * BM + r_local];
-                A.out_vals[row * A.kc + half * KH + k] = lv[k * BM + r_local];
+            for (int k = 0; k < KC; k++) {
+                A.out_ids[row * KC + k] = li[k * BM + r_local];
+                A.out_vals[row * KC + k] = lv[k * BM + r_local];
             }
         }
     }
@@ -369,10 +364,9 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     using namespace knn;
     static const int debug = getenv("PW_KNN_DEBUG") ? atoi(getenv("PW_KNN_DEBUG")) : 0;
     if (nq <= 0) return 0;
-    if (!q || !x || !xn || !out_ids || !out_vals || n <= 0 || d < 1 || kc < 2 || kc > 64 || kc % 2 ||
-        n >= (1ll << 31) ||
+    if (!q || !x || !xn || !out_ids || !out_vals || n <= 0 || d < 1 || kc < 1 || kc > 64 || n >= (1ll << 31) ||
         nq >= (1ll << 31) || (d * 4) % 16 != 0) {
-        snprintf(msg, 256, "knn screen: unsupported arguments (d %% 4 == 0, even 2 <= kc <= 64, n < 2^31)");
+        snprintf(msg, 256, "knn screen: unsupported arguments (d %% 4 == 0, 1 <= kc <= 64, n < 2^31)");
         return -1;
     }
     const int ka = (d + 31) / 32;
@@ -385,9 +379,9 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     const size_t a_bytes = (size_t)BM * ka * ATOM;
     const size_t lists = (size_t)kc * BM * 8;
     int bn = 0, st = 0;
-    for (int cand_bn : {128, 64})  // >= 64: each epilogue warp takes whole 32-column chunks
+    for (int cand_bn : {128, 64, 32})
         for (int cand_st : {4, 3, 2}) {
-            const size_t need = a_bytes + (size_t)cand_st * cand_bn * ka * ATOM + 1024 + lists + 2048;
+            const size_t need = a_bytes + (size_t)cand_st * cand_bn * ka * ATOM + 1024 + lists + 2048 + 32 * BM * 4;
             if (!bn && need <= (size_t)optin) {
                 bn = cand_bn;
                 st = cand_st;
@@ -424,7 +418,8 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     off += (size_t)kc * BM * 4;
     A.o_nb = (uint32_t)off;
     off += (size_t)2 * bn * 4;
-
+    A.o_scr = (uint32_t)off;
+    off += (size_t)32 * BM * 4;
     CUtensorMap tq, tx;
     if (!knn_map(&tq, q, nq, d, BM) || !knn_map(&tx, x, n, d, bn)) {
         snprintf(msg, 256, "knn screen: cuTensorMapEncodeTiled failed");

@@ -113,7 +113,7 @@ def knn_screen_tc(base: torch.Tensor, queries: torch.Tensor, kc: int, self_off: 
 
 
 def _certify(queries: torch.Tensor, base_norm_max: float, vals: torch.Tensor, kth_exact: torch.Tensor,
-             full: torch.Tensor | None = None) -> torch.Tensor:
+             full: torch.Tensor) -> torch.Tensor:
     """Rows whose exact top-k provably lies inside the screened candidates.
 
     Every non-candidate c has a screened value a_c >= tau (the list's worst),
@@ -127,21 +127,12 @@ def _certify(queries: torch.Tensor, base_norm_max: float, vals: torch.Tensor, kt
     q64 = queries.double()
     qn2 = (q64 * q64).sum(1)
     qn = qn2.sqrt()
-    # K4 returns two half-lists per row (one per column half of every tile):
-    # a non-candidate column is >= the worst entry of the list of its half,
-    # so the bound is the smaller of the two lists' worst values; a list that
-    # is not full holds every column of its half (no non-candidates there)
-    h = vals.shape[1] // 2
-    taus = []
-    for part in (vals[:, :h], vals[:, h:]):
-        worst = torch.where(torch.isfinite(part), part, torch.full_like(part, -float("inf"))).max(1).values
-        taus.append(torch.where(torch.isfinite(part).all(1), worst, torch.full_like(worst, float("inf"))))
-    tau = torch.minimum(taus[0], taus[1]).double()
+    tau = torch.where(torch.isfinite(vals), vals, torch.full_like(vals, -float("inf"))).max(1).values.double()
     dk = kth_exact.double()
     R = torch.clamp(qn + dk.clamp(min=0).sqrt() + 1e-3, max=float(base_norm_max) + 1e-3)
     E = TC_ERR * qn * R + 2.0 ** -15 * (2 * R * R + 2 * qn * R)
     ok = (qn2 + tau - E) * (1 - 2.0 ** -20) > dk * (1 + 2.0 ** -20)
-    return ok | torch.isinf(tau)  # both lists short: every other row is a candidate
+    return ok | ~full  # a list that is not full holds every other row
 
 
 def _rescore_rank(base, queries, cand, k, exclude_self):
@@ -176,7 +167,6 @@ def exact_topk(base: torch.Tensor, queries: torch.Tensor, k: int, exclude_self: 
         cand = _screen(base, queries, kc)
         return _rescore_rank(base, queries, cand, k, exclude_self)
     kc = min(64, max(kc, k + 32))
-    kc += kc % 2  # two half-lists
     t0 = time.perf_counter()
     # the screen sees centred rows: distances are translation invariant and
     # the TF32 error bound scales with |q| |x|, so this tightens certification
@@ -188,7 +178,8 @@ def exact_topk(base: torch.Tensor, queries: torch.Tensor, k: int, exclude_self: 
         torch.cuda.synchronize(base.device)
         t1 = time.perf_counter()
     ids, sq = _rescore_rank(base, queries, cand, k, exclude_self)
-    ok = _certify(qc, float(xn.max().sqrt()), vals, sq[:, k - 1])
+    full = (cand >= 0).all(1)
+    ok = _certify(qc, float(xn.max().sqrt()), vals, sq[:, k - 1], full)
     del bc, qc
     redo = torch.nonzero(~ok).flatten()
     if stats is not None:
