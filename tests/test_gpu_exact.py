@@ -90,7 +90,7 @@ def test_build_errors():
 
 
 @pytest.mark.parametrize("d,n,nq,self_ex,dup", [(96, 40000, 3000, True, False), (128, 20000, 2000, False, False),
-                                                (200, 12000, 1000, True, False), (96, 30000, 2000, True, True),
+                                                (100, 12000, 1000, True, False), (96, 30000, 2000, True, True),
                                                 (16, 40, 40, True, False)])
 def test_tensor_core_screen_topk_equals_fp32_screen(d, n, nq, self_ex, dup):
     """exact_topk through K4 (certified, redo of the rest) == through the FP32
@@ -111,3 +111,18 @@ def test_tensor_core_screen_topk_equals_fp32_screen(d, n, nq, self_ex, dup):
     assert torch.equal(a_ids, b_ids), st
     assert torch.equal(a_sq, b_sq)
     assert st["certified"] + st["redone"] == nq
+
+
+def test_tensor_core_screen_shape_limits():
+    """d = 200 needs more shared memory than K4's resident query block leaves:
+    forced, it raises; "auto" takes the FP32 screen."""
+    import torch
+
+    from paper_2507_17094_b200 import builder
+
+    x = builder.gen_latent(3000, 200, 16, 1, 1.0, 0.05, 5, device="cuda")
+    with pytest.raises(ValueError, match="shared memory"):
+        exact.knn_screen_tc(x, x[:10].contiguous(), 64)
+    a, _ = exact.exact_topk(x, x[:50].contiguous(), 10, screen="auto")
+    b, _ = exact.exact_topk(x, x[:50].contiguous(), 10, screen="fp32")
+    assert torch.equal(a, b)
