@@ -78,18 +78,14 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
                   bdir / "knn_screen.o"),
                  ([nv, *CFLAGS, *extra, "-c", str(CSRC / "gather_probe.cu"), "-o", str(bdir / "gather_probe.o")],
                   bdir / "gather_probe.o")]
-    for d in DIMS:
-        obj = bdir / f"k_{d}.o"
-        jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-c", str(CSRC / "k_inst.cu"), "-o",
-                           str(obj)], obj))
-    for d in DIMS_U8:
-        obj = bdir / f"k_u8_{d}.o"
-        jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-DPW_U8", "-c", str(CSRC / "k_inst.cu"),
-                           "-o", str(obj)], obj))
-    for d in DIMS_IP:
-        obj = bdir / f"k_ip_{d}.o"
-        jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", "-DPW_IP", "-c", str(CSRC / "k_inst.cu"),
-                           "-o", str(obj)], obj))
+    # every specialised d also gets its FAST instance (-DPW_FAST, cold paths
+    # compiled out; the host picks it per launch)
+    for kind, dims, flag in (("", DIMS, []), ("u8_", DIMS_U8, ["-DPW_U8"]), ("ip_", DIMS_IP, ["-DPW_IP"])):
+        for d in dims:
+            for fast in ((False, True) if d else (False,)):
+                obj = bdir / f"k_{kind}{'f_' if fast else ''}{d}.o"
+                jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", *flag, *(["-DPW_FAST"] if fast else []),
+                                   "-c", str(CSRC / "k_inst.cu"), "-o", str(obj)], obj))
     workers = jobs or max(1, min(len(jobs_list), os.cpu_count() or 1))
     with ThreadPoolExecutor(workers) as pool:
         logs = list(pool.map(lambda j: _run(j[0]), jobs_list))

@@ -878,9 +878,15 @@ static __device__ __forceinline__ int visited_lossy(const KArgs& A, WarpState& S
 // GLOBAL_ONLY (the specialised kernels): the shared table is skipped and every
 // probe goes to the per-warp epoch table, so only the batched-probe path below
 // is compiled into the hot loop.
-template <bool GLOBAL_ONLY>
+// FAST kernel instances (host-selected per launch, prepare()): the launch
+// uses the lossy visited cache, full or direction-guided selection and
+// degrees <= 32, so the exact visited path, the random-selection arm and the
+// shared-memory DGS path for wide degrees are compiled out -- 19% less code
+// in the hot loop's address range, measured 6% (PathWeaver) / 2% (naive)
+// faster at the C2 bench point (profiles/r02/ab_cold_r02z.log).
+template <bool GLOBAL_ONLY, bool FAST = false>
 __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
-    if (A.lossy) return visited_lossy(A, S, nb);
+    if (FAST || A.lossy) return visited_lossy(A, S, nb);
     const unsigned lane = lane_id();
     if (!GLOBAL_ONLY && !S.ovf && S.vcount + nb > A.vis_limit) S.ovf = true;
     int cnt = 0;
@@ -1468,7 +1474,7 @@ __device__ __forceinline__ void prefetch_parents(const KArgs& A, const WarpState
 
 // _expand (search.py:235-266) up to the ordered candidate list in S.cand;
 // returns the candidate count p * n_sel.
-template <int D, typename VT>
+template <int D, typename VT, bool FAST = false>
 __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                       const int32_t* parents, int np, int it, Pcg64& rng) {
     const unsigned lane = lane_id();
@@ -1626,7 +1632,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                     if ((int)lane < j && rank < nsel)
                         S.cand[(pg + pi) * nsel + rank] = craw[(pg + pi) * j + lane];
                 }
-            } else {
+            } else if (!FAST) {
                 for (int pi = 0; pi < gp; pi++)
                     for (int w = 0; w < W; w++) {
                         int t = 32 * w + (int)lane;
@@ -1656,7 +1662,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
             }
             __syncwarp();
         }
-    } else {
+    } else if (!FAST) {
         fetch_group(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
             dst = craw + r * j;
             src = G.adj + (size_t)parents[r] * j;
@@ -1703,7 +1709,7 @@ static __device__ __noinline__ int64_t log_visits(int32_t* log, int64_t cap, con
 // One full search (search.py:269-335) over graph G.  Seeds (already in
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
-template <int D, typename VT, int M>
+template <int D, typename VT, int M, bool FAST = false>
 __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                            int ns, bool fill_random, Pcg64& rng, int64_t task,
                            int64_t* n_logged) {
@@ -1779,7 +1785,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         nb = cnt;
     }
     bh_clear(A, S);
-    int n_new = visited_filter<(D > 0)>(A, S, nb);
+    int n_new = visited_filter<(D > 0), FAST>(A, S, nb);
     PW_T(0);
 
     bool converged = false;
@@ -1820,7 +1826,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
             break;
         }
         S.c_ne += np;
-        int nc = expand<D, VT>(A, S, G, C, parents, np, it, rng);
+        int nc = expand<D, VT, FAST>(A, S, G, C, parents, np, it, rng);
         PW_T(4);
         bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
         if (nc <= C.cap && !C.log)
@@ -1830,14 +1836,14 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         S.c_tv += nb;
         bh_clear(A, S);
         PW_T(5);
-        n_new = visited_filter<(D > 0)>(A, S, nb);
+        n_new = visited_filter<(D > 0), FAST>(A, S, nb);
         PW_T(6);
     }
     PW_T(7);
     return converged;
 }
 
-template <int D, typename VT, int M>
+template <int D, typename VT, int M, bool FAST = false>
 __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const unsigned lane = lane_id();
@@ -1995,7 +2001,7 @@ __global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __
                 rng = A.rng_io ? A.rng_io[task]
                                : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)tsk[0], (uint64_t)tsk[1]));
             }
-            converged = run_search<D, VT, M>(A, S, gph ? A.ghost : G, (&A.cfg)[gph ? 2 : (tsk[1] > 0 ? 1 : 0)],
+            converged = run_search<D, VT, M, FAST>(A, S, gph ? A.ghost : G, (&A.cfg)[gph ? 2 : (tsk[1] > 0 ? 1 : 0)],
                                              ns, fill_random, rng, task, &n_logged);
             if (gph) {
                 if (lane == 0) S.cand[0] = A.ghost.gid[(uint32_t)S.qk_cur()[0]];

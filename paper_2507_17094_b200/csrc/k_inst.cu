@@ -10,10 +10,18 @@
 #define PW_CAT2(a, b) a##b
 #define PW_CAT(a, b) PW_CAT2(a, b)
 
-#if defined(PW_U8)
-pw::KernelFn PW_CAT(pw_kernel_u8_, PW_DIM)() { return pw::beam_search_kernel<PW_DIM, uint8_t, 0>; }
-#elif defined(PW_IP)
-pw::KernelFn PW_CAT(pw_kernel_ip_, PW_DIM)() { return pw::beam_search_kernel<PW_DIM, float, 1>; }
+// -DPW_FAST: the FAST instance (cold paths compiled out, beam_search.cuh)
+#if defined(PW_FAST)
+#define PW_FAST_V true
+#define PW_SFX(name) PW_CAT(name, f_)
 #else
-pw::KernelFn PW_CAT(pw_kernel_, PW_DIM)() { return pw::beam_search_kernel<PW_DIM, float, 0>; }
+#define PW_FAST_V false
+#define PW_SFX(name) name
+#endif
+#if defined(PW_U8)
+pw::KernelFn PW_CAT(PW_SFX(pw_kernel_u8_), PW_DIM)() { return pw::beam_search_kernel<PW_DIM, uint8_t, 0, PW_FAST_V>; }
+#elif defined(PW_IP)
+pw::KernelFn PW_CAT(PW_SFX(pw_kernel_ip_), PW_DIM)() { return pw::beam_search_kernel<PW_DIM, float, 1, PW_FAST_V>; }
+#else
+pw::KernelFn PW_CAT(PW_SFX(pw_kernel_), PW_DIM)() { return pw::beam_search_kernel<PW_DIM, float, 0, PW_FAST_V>; }
 #endif

@@ -89,9 +89,9 @@ bool make_plan(int d, L2Plan& P) {
 #define PW_DIMS_IP(X) X(96) X(128) X(200)
 typedef KernelFn kernel_fn;
 }  // namespace
-#define PW_DECL(v) KernelFn pw_kernel_##v();
-#define PW_DECL_U8(v) KernelFn pw_kernel_u8_##v();
-#define PW_DECL_IP(v) KernelFn pw_kernel_ip_##v();
+#define PW_DECL(v) KernelFn pw_kernel_##v(); KernelFn pw_kernel_f_##v();
+#define PW_DECL_U8(v) KernelFn pw_kernel_u8_##v(); KernelFn pw_kernel_u8_f_##v();
+#define PW_DECL_IP(v) KernelFn pw_kernel_ip_##v(); KernelFn pw_kernel_ip_f_##v();
 PW_DIMS(PW_DECL)
 PW_DIMS_U8(PW_DECL_U8)
 PW_DIMS_IP(PW_DECL_IP)
@@ -102,12 +102,14 @@ KernelFn pw_kernel_ip_0();
 #undef PW_DECL_U8
 #undef PW_DECL_IP
 namespace {
-kernel_fn pick_kernel(int d, int dtype, int metric) {
+// fast: the FAST instance of a specialised d (beam_search.cuh); the generic
+// instance has none
+kernel_fn pick_kernel(int d, int dtype, int metric, bool fast = false) {
     if (metric == PW_METRIC_IP) {
         switch (d) {
 #define PW_CASE(v) \
     case v:        \
-        return pw_kernel_ip_##v();
+        return fast ? pw_kernel_ip_f_##v() : pw_kernel_ip_##v();
             PW_DIMS_IP(PW_CASE)
 #undef PW_CASE
             default:
@@ -118,7 +120,7 @@ kernel_fn pick_kernel(int d, int dtype, int metric) {
         switch (d) {
 #define PW_CASE(v) \
     case v:        \
-        return pw_kernel_u8_##v();
+        return fast ? pw_kernel_u8_f_##v() : pw_kernel_u8_##v();
             PW_DIMS_U8(PW_CASE)
 #undef PW_CASE
             default:
@@ -128,7 +130,7 @@ kernel_fn pick_kernel(int d, int dtype, int metric) {
     switch (d) {
 #define PW_CASE(v) \
     case v:        \
-        return pw_kernel_##v();
+        return fast ? pw_kernel_f_##v() : pw_kernel_##v();
         PW_DIMS(PW_CASE)
 #undef PW_CASE
         default:
@@ -195,16 +197,22 @@ int dev_info(int dev, DevInfo** out) {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
 #define PW_ATTR(v)                                                                             \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_##v(),                                 \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_f_##v(),                               \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS(PW_ATTR)
 #undef PW_ATTR
 #define PW_ATTR(v)                                                                             \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_##v(),                              \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_f_##v(),                            \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS_U8(PW_ATTR)
 #undef PW_ATTR
 #define PW_ATTR(v)                                                                             \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_##v(),                              \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_f_##v(),                            \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS_IP(PW_ATTR)
 #undef PW_ATTR
@@ -776,6 +784,11 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         gsz = slots / 2;  // u64 words of the per-warp region
     }
     A.gmask = (int32_t)(gsz - 1);
+    // the FAST K1 instance when this launch never needs the cold paths it
+    // drops: lossy visited cache, no random selection, degrees <= 32
+    if (specialised && lossy && A.cfg.prune_sel != PW_SEL_RANDOM && A.cfg_late.prune_sel != PW_SEL_RANDOM &&
+        G.j <= 32 && (!ghost_on || sh->gj <= 32) && !(PW_TMA_ROWS && A.tma_rows))
+        Lc.fn = pick_kernel(d, sh->dtype, p.metric, true);
     int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
     int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
     std::lock_guard<std::mutex> lk(sh->mu);
