@@ -1422,7 +1422,7 @@ static __device__ __noinline__ void copy_issue_wait(const uint4* desc, int n_row
 // Fetch up to 3 row sets (adjacency, parent vectors, direction rows) for the
 // parents in ONE round trip: lanes write one descriptor per row, then a single
 // out-of-line issuer runs TMA bulk copies (aligned rows) or cp.async.
-template <typename F>
+template <bool FAST = false, typename F>
 __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_rows, uint32_t total,
                                             F&& row, bool wait = true) {
     const unsigned lane = lane_id();
@@ -1435,7 +1435,9 @@ __device__ __forceinline__ void fetch_group(const KArgs& A, WarpState& S, int n_
         S.desc[r] = make_uint4(smem_u32(dst), bytes, (uint32_t)sp, (uint32_t)(sp >> 32));
     }
     __syncwarp();
-    if (A.bulk_adj == 2)
+    if (FAST)  // FAST launches have 16-byte rows and no TMA bulk expansion (prepare())
+        copy16_issue_wait(S.desc, n_rows, wait);
+    else if (A.bulk_adj == 2)
         S.phase = bulk_issue_wait(S.desc, S.mbar + 2, S.phase, n_rows, total);
     else if (A.bulk_adj)
         copy16_issue_wait(S.desc, n_rows, wait);
@@ -1483,7 +1485,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
     const bool prune = C.prune_sel != 0 && it < C.cool_start;
     const uint32_t adj_bytes = (uint32_t)j * 4u;
     if (!prune) {
-        fetch_group(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
+        fetch_group<FAST>(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
             dst = S.cand + r * j;
             src = G.adj + (size_t)parents[r] * j;
             b = adj_bytes;
@@ -1515,7 +1517,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                 constexpr int CH = D / 4;  // float4 chunks per row
                 // cp.async of the adjacency + direction rows issued first
                 // (no wait), then the parent rows' register loads: one round trip
-                fetch_group(A, S, 2 * gp, gp * (adj_bytes + dir_bytes),
+                fetch_group<FAST>(A, S, 2 * gp, gp * (adj_bytes + dir_bytes),
                             [&](int r, void*& dst, const void*& src, uint32_t& b) {
                                 const int pi = r % gp;
                                 const int32_t par = parents[pg + pi];
@@ -1559,7 +1561,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                 }
                 __syncwarp();
             } else
-            fetch_group(A, S, 3 * gp, gp * (adj_bytes + vec_bytes + dir_bytes),
+            fetch_group<FAST>(A, S, 3 * gp, gp * (adj_bytes + vec_bytes + dir_bytes),
                         [&](int r, void*& dst, const void*& src, uint32_t& b) {
                             const int pi = r % gp, kind = r / gp;
                             const int32_t par = parents[pg + pi];
@@ -1663,7 +1665,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
             __syncwarp();
         }
     } else if (!FAST) {
-        fetch_group(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
+        fetch_group<FAST>(A, S, np, np * adj_bytes, [&](int r, void*& dst, const void*& src, uint32_t& b) {
             dst = craw + r * j;
             src = G.adj + (size_t)parents[r] * j;
             b = adj_bytes;
@@ -1793,9 +1795,9 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     for (int it = 0; it < C.max_iter; it++) {
         S.c_it++;
         int inserted = 0;
-        if (A.prefetch && it > 0 && it < C.max_iter - 1) prefetch_parents<D, VT>(A, S, G, C);
+        if (!FAST && A.prefetch && it > 0 && it < C.max_iter - 1) prefetch_parents<D, VT>(A, S, G, C);
         if (n_new) {
-            if (C.log && A.visit_log)
+            if (!FAST && C.log && A.visit_log)
                 *n_logged = log_visits(A.visit_log + task * A.visit_cap, A.visit_cap, S.newl, n_new, *n_logged);
             S.c_dc += n_new;
             PW_T(7);
@@ -1829,7 +1831,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         int nc = expand<D, VT, FAST>(A, S, G, C, parents, np, it, rng);
         PW_T(4);
         bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
-        if (nc <= C.cap && !C.log)
+        if (FAST || (nc <= C.cap && !C.log))  // FAST: no buffer_cap, no visit log
             nb = dedup_unordered(A, S, S.cand, nc, S.newl);
         else
             nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);

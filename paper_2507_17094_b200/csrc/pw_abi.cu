@@ -787,7 +787,8 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
     // the FAST K1 instance when this launch never needs the cold paths it
     // drops: lossy visited cache, no random selection, degrees <= 32
     if (specialised && lossy && A.cfg.prune_sel != PW_SEL_RANDOM && A.cfg_late.prune_sel != PW_SEL_RANDOM &&
-        G.j <= 32 && (!ghost_on || sh->gj <= 32) && !(PW_TMA_ROWS && A.tma_rows))
+        G.j <= 32 && (!ghost_on || sh->gj <= 32) && !(PW_TMA_ROWS && A.tma_rows) && !p.buffer_cap &&
+        !A.prefetch && A.bulk_adj == 1)
         Lc.fn = pick_kernel(d, sh->dtype, p.metric, true);
     int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
     int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
