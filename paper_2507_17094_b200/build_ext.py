@@ -82,9 +82,10 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None,
     # compiled out; the host picks it per launch)
     for kind, dims, flag in (("", DIMS, []), ("u8_", DIMS_U8, ["-DPW_U8"]), ("ip_", DIMS_IP, ["-DPW_IP"])):
         for d in dims:
-            for fast in ((False, True) if d else (False,)):
-                obj = bdir / f"k_{kind}{'f_' if fast else ''}{d}.o"
-                jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", *flag, *(["-DPW_FAST"] if fast else []),
+            for var, vflags in ((("", []), ("f_", ["-DPW_FAST"]), ("fw_", ["-DPW_FAST", "-DPW_WIDE"]))
+                                 if d else (("", []),)):
+                obj = bdir / f"k_{kind}{var}{d}.o"
+                jobs_list.append(([nv, *CFLAGS, *extra, f"-DPW_DIM={d}", *flag, *vflags,
                                    "-c", str(CSRC / "k_inst.cu"), "-o", str(obj)], obj))
     workers = jobs or max(1, min(len(jobs_list), os.cpu_count() or 1))
     with ThreadPoolExecutor(workers) as pool:

@@ -30,6 +30,7 @@
 
 namespace pw {
 constexpr int kMaxWarps = PW_MAX_THREADS / 32;
+constexpr int kWideWarps = 20;  // the FAST direction-guided build: 640 threads, 96 registers
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 constexpr int kMaxLeaves = 64;
@@ -1845,8 +1846,8 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
     return converged;
 }
 
-template <int D, typename VT, int M, bool FAST = false>
-__global__ void __launch_bounds__(PW_MAX_THREADS, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
+template <int D, typename VT, int M, bool FAST = false, int MAXT = PW_MAX_THREADS>
+__global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_constant__ KArgs A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;

@@ -11,7 +11,11 @@
 #define PW_CAT(a, b) PW_CAT2(a, b)
 
 // -DPW_FAST: the FAST instance (cold paths compiled out, beam_search.cuh)
-#if defined(PW_FAST)
+// -DPW_FAST -DPW_WIDE: its 20-warp build (kWideWarps x 32 threads)
+#if defined(PW_FAST) && defined(PW_WIDE)
+#define PW_FAST_V true, pw::kWideWarps * 32
+#define PW_SFX(name) PW_CAT(name, fw_)
+#elif defined(PW_FAST)
 #define PW_FAST_V true
 #define PW_SFX(name) PW_CAT(name, f_)
 #else

@@ -89,9 +89,9 @@ bool make_plan(int d, L2Plan& P) {
 #define PW_DIMS_IP(X) X(96) X(128) X(200)
 typedef KernelFn kernel_fn;
 }  // namespace
-#define PW_DECL(v) KernelFn pw_kernel_##v(); KernelFn pw_kernel_f_##v();
-#define PW_DECL_U8(v) KernelFn pw_kernel_u8_##v(); KernelFn pw_kernel_u8_f_##v();
-#define PW_DECL_IP(v) KernelFn pw_kernel_ip_##v(); KernelFn pw_kernel_ip_f_##v();
+#define PW_DECL(v) KernelFn pw_kernel_##v(); KernelFn pw_kernel_f_##v(); KernelFn pw_kernel_fw_##v();
+#define PW_DECL_U8(v) KernelFn pw_kernel_u8_##v(); KernelFn pw_kernel_u8_f_##v(); KernelFn pw_kernel_u8_fw_##v();
+#define PW_DECL_IP(v) KernelFn pw_kernel_ip_##v(); KernelFn pw_kernel_ip_f_##v(); KernelFn pw_kernel_ip_fw_##v();
 PW_DIMS(PW_DECL)
 PW_DIMS_U8(PW_DECL_U8)
 PW_DIMS_IP(PW_DECL_IP)
@@ -104,12 +104,12 @@ KernelFn pw_kernel_ip_0();
 namespace {
 // fast: the FAST instance of a specialised d (beam_search.cuh); the generic
 // instance has none
-kernel_fn pick_kernel(int d, int dtype, int metric, bool fast = false) {
+kernel_fn pick_kernel(int d, int dtype, int metric, bool fast = false, bool wide = false) {
     if (metric == PW_METRIC_IP) {
         switch (d) {
 #define PW_CASE(v) \
     case v:        \
-        return fast ? pw_kernel_ip_f_##v() : pw_kernel_ip_##v();
+        return fast ? (wide ? pw_kernel_ip_fw_##v() : pw_kernel_ip_f_##v()) : pw_kernel_ip_##v();
             PW_DIMS_IP(PW_CASE)
 #undef PW_CASE
             default:
@@ -120,7 +120,7 @@ kernel_fn pick_kernel(int d, int dtype, int metric, bool fast = false) {
         switch (d) {
 #define PW_CASE(v) \
     case v:        \
-        return fast ? pw_kernel_u8_f_##v() : pw_kernel_u8_##v();
+        return fast ? (wide ? pw_kernel_u8_fw_##v() : pw_kernel_u8_f_##v()) : pw_kernel_u8_##v();
             PW_DIMS_U8(PW_CASE)
 #undef PW_CASE
             default:
@@ -130,7 +130,7 @@ kernel_fn pick_kernel(int d, int dtype, int metric, bool fast = false) {
     switch (d) {
 #define PW_CASE(v) \
     case v:        \
-        return fast ? pw_kernel_f_##v() : pw_kernel_##v();
+        return fast ? (wide ? pw_kernel_fw_##v() : pw_kernel_f_##v()) : pw_kernel_##v();
         PW_DIMS(PW_CASE)
 #undef PW_CASE
         default:
@@ -199,21 +199,24 @@ int dev_info(int dev, DevInfo** out) {
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_##v(),                                 \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_f_##v(),                               \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_fw_##v(), cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS(PW_ATTR)
 #undef PW_ATTR
 #define PW_ATTR(v)                                                                             \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_##v(),                              \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_f_##v(),                            \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_u8_fw_##v(), cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS_U8(PW_ATTR)
 #undef PW_ATTR
 #define PW_ATTR(v)                                                                             \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_##v(),                              \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
     PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_f_##v(),                            \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin)); \
+    PW_CUDA(cudaFuncSetAttribute((const void*)pw_kernel_ip_fw_##v(), cudaFuncAttributeMaxDynamicSharedMemorySize, I.smem_optin));
         PW_DIMS_IP(PW_ATTR)
 #undef PW_ATTR
         I.attr_set = true;
@@ -756,7 +759,19 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
                      ? ((tun && (tun->flags & 4)) ? 2 : 1)
                      : 0;
 
-    int wpb = (int)std::min<int64_t>(kMaxWarps, I->smem_optin / off);
+    // the FAST K1 instance when this launch never needs the cold paths it
+    // drops: lossy visited cache, no random selection, degrees <= 32; for
+    // direction-guided launches its 20-warp build (96 registers; measured 3%
+    // faster for PathWeaver, 3% slower for full selection, ab_warps_r02ad.log)
+    const bool lossy_req = tun && (tun->flags & 2) && !p.log_visits;
+    const bool fast = specialised && lossy_req && A.cfg.prune_sel != PW_SEL_RANDOM &&
+                      A.cfg_late.prune_sel != PW_SEL_RANDOM && G.j <= 32 && (!ghost_on || sh->gj <= 32) &&
+                      !(PW_TMA_ROWS && A.tma_rows) && !p.buffer_cap && !A.prefetch && A.bulk_adj == 1;
+    const bool wide = fast && A.cfg.prune_sel == PW_SEL_DIRECTION && !(tun && tun->warps_per_sm > 0 &&
+                                                                       tun->warps_per_sm <= kMaxWarps);
+    if (fast) Lc.fn = pick_kernel(d, sh->dtype, p.metric, true, wide);
+    const int max_w = wide ? kWideWarps : kMaxWarps;
+    int wpb = (int)std::min<int64_t>(max_w, I->smem_optin / off);
     if (tun && tun->warps_per_sm > 0) wpb = std::min(wpb, tun->warps_per_sm);
     if (wpb < 1) return set_err(PW_EINVAL, "search configuration needs " + std::to_string(off) +
                                               " bytes of shared memory per query (l or degree too large)");
@@ -784,12 +799,6 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
         gsz = slots / 2;  // u64 words of the per-warp region
     }
     A.gmask = (int32_t)(gsz - 1);
-    // the FAST K1 instance when this launch never needs the cold paths it
-    // drops: lossy visited cache, no random selection, degrees <= 32
-    if (specialised && lossy && A.cfg.prune_sel != PW_SEL_RANDOM && A.cfg_late.prune_sel != PW_SEL_RANDOM &&
-        G.j <= 32 && (!ghost_on || sh->gj <= 32) && !(PW_TMA_ROWS && A.tma_rows) && !p.buffer_cap &&
-        !A.prefetch && A.bulk_adj == 1)
-        Lc.fn = pick_kernel(d, sh->dtype, p.metric, true);
     int64_t want_max = std::max(A.cfg.want, A.gcfg.want);
     int64_t scr = std::max<int64_t>(next_pow2(4 * want_max + 8) * 2, next_pow2((int64_t)(1.2 * want_max) + 1));
     std::lock_guard<std::mutex> lk(sh->mu);
