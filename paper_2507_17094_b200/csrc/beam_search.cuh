@@ -138,6 +138,12 @@ struct KArgs {
     // task waits for its entry, which shard g-1 stores straight into this
     // shard's inbox (P2P over NVLink between GPUs) when its stage s-1 search
     // ends -- no stage barriers, no host round trips (pipeline.py:327-347).
+    // Overlapped query upload (pw_run): query rows arrive in chunks of
+    // q_chunk rows on a copy stream, each chunk's flag set to q_epoch after it
+    // lands; a task polls its chunk's flag before reading its row.
+    const uint32_t* qready;  // or null (queries already resident)
+    int32_t q_chunk;
+    uint32_t q_epoch;
     int32_t df;             // 1: dataflow task mapping
     int32_t df_g, df_N;
     int32_t df_lo[9];       // chunk bounds, np.array_split(arange(Q), N) (pipeline.py:327)
@@ -151,6 +157,11 @@ struct KArgs {
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -1927,6 +1938,20 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
                 n_ent = A.fwd;
                 __syncwarp();
             }
+        }
+        if (A.qready) {
+            // overlapped upload: wait (bounded) for this row's chunk to land
+            if (lane == 0) {
+                const uint32_t* f = A.qready + (A.df ? row : A.q0 + row) / A.q_chunk;
+                for (uint32_t spin = 0; ld_acquire_gpu_u32(f) != A.q_epoch; spin++) {
+                    if (spin > (1u << 25)) {
+                        atomicOr(A.err, 64);
+                        break;
+                    }
+                    __nanosleep(128);
+                }
+            }
+            __syncwarp();
         }
         // query row -> smem
         for (int t = lane; t < A.d; t += 32) S.q[t] = A.queries[(size_t)row * A.d + t];

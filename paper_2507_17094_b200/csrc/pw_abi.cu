@@ -467,6 +467,23 @@ int make_row_tensor_map(CUtensorMap* tm, const void* base, int64_t n, int32_t d,
     return 0;
 }
 
+// cuStreamWriteValue32 through the runtime's driver entry point: a 32-bit
+// store executed by the stream itself after its preceding copies (no kernel,
+// so it cannot wait behind a persistent K1 that holds every SM)
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32Fn write_value32() {
+    static WriteValue32Fn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<WriteValue32Fn>(p);
+    });
+    return fn;
+}
+
 SearchCfg make_cfg(const pw_params& p, int64_t n, int32_t j) {
     SearchCfg c;
     c.k = p.k;
@@ -856,7 +873,8 @@ int check_err(pw_shard* sh) {
     PW_CUDA(cudaMemcpy(&e, sh->counter + 1, sizeof e, cudaMemcpyDeviceToHost));
     if (e) {
         cudaMemset(sh->counter + 1, 0, sizeof(int32_t));
-        return set_err(PW_ECUDA, (e & 16)   ? std::string("dataflow inbox wait timed out (flag ") + std::to_string(e) + ")"
+        return set_err(PW_ECUDA, (e & 64)   ? std::string("query upload wait timed out (flag ") + std::to_string(e) + ")"
+                                 : (e & 16) ? std::string("dataflow inbox wait timed out (flag ") + std::to_string(e) + ")"
                                  : (e & 32) ? std::string("TMA gather never completed (flag ") + std::to_string(e) + ")"
                                             : "beam_search_kernel internal table overflow (flag " + std::to_string(e) + ")");
     }
@@ -970,6 +988,15 @@ int pw_shard_destroy(pw_shard* sh) {
 
 int64_t pw_shard_bytes(const pw_shard* sh) { return sh ? sh->bytes : 0; }
 
+// Overlapped query upload of the current pw_run call (this thread), read by
+// the launch builders below; null outside pw_run.
+struct QUpload {
+    const uint32_t* flags;
+    int32_t chunk;
+    uint32_t epoch;
+};
+thread_local const QUpload* tl_upload = nullptr;
+
 int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuning,
                     const float* queries, int64_t q0, int64_t n, int32_t stage,
                     const int32_t* entries_in, int32_t* forward_out, int32_t* shard_ids,
@@ -987,6 +1014,11 @@ int pw_search_stage(pw_shard* sh, const pw_params* params, const pw_tuning* tuni
     A.q0 = q0;
     A.n_tasks = (int32_t)n;
     A.queries = queries + q0 * sh->d;
+    if (tl_upload) {
+        A.qready = tl_upload->flags;
+        A.q_chunk = tl_upload->chunk;
+        A.q_epoch = tl_upload->epoch;
+    }
     A.entries = entries_in ? entries_in + q0 * A.fwd : nullptr;
     A.forward = forward_out ? forward_out + q0 * A.fwd : nullptr;
     const int64_t k = params->k;
@@ -1032,6 +1064,11 @@ int pw_search_dataflow(pw_shard* sh, const pw_params* params, const pw_tuning* t
     A.q0 = 0;
     A.n_tasks = (int32_t)q;
     A.queries = queries;
+    if (tl_upload) {
+        A.qready = tl_upload->flags;
+        A.q_chunk = tl_upload->chunk;
+        A.q_epoch = tl_upload->epoch;
+    }
     A.entries = nullptr;
     A.forward = nullptr;
     const int64_t k = params->k;
@@ -1187,6 +1224,11 @@ struct RunWs {
     uint64_t* inbox = nullptr;
     size_t inbox_cap = 0;  // u64 words
     uint32_t epoch = 0;
+    // overlapped query upload (pw_run): copy stream, chunk flags, call tag
+    cudaStream_t cs = nullptr;
+    uint32_t* qflags = nullptr;
+    size_t qflags_cap = 0;
+    uint32_t qepoch = 0;
 };
 RunWs g_ws[64];
 
@@ -1360,10 +1402,45 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     int32_t* s32 = (int32_t*)(b + o_s32);
     int64_t* s64 = (int64_t*)(b + o_s64);
     int32_t* err = (int32_t*)(b + o_err);
-    PW_CUDA(cudaMemcpyAsync(dq, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
+    // Query upload overlapped with K1: chunks of kChunk rows on a copy stream,
+    // each followed by a stream-ordered flag store (cuStreamWriteValue32) that
+    // the kernel polls before reading a row of that chunk.  Without the driver
+    // entry point: one copy ahead of the kernel on the same stream.
+    constexpr int32_t kChunk = 512;
+    const int64_t n_chunks = (q + kChunk - 1) / kChunk;
+    WriteValue32Fn wv = write_value32();
+    QUpload up{};
+    if (wv && q > kChunk) {
+        if (!W.cs) PW_CUDA(cudaStreamCreateWithFlags(&W.cs, cudaStreamNonBlocking));
+        if (W.qflags_cap < (size_t)n_chunks) {
+            if (W.qflags) cudaFree(W.qflags);
+            W.qflags = nullptr;
+            W.qflags_cap = 0;
+            PW_CUDA(cudaMalloc(&W.qflags, sizeof(uint32_t) * n_chunks));
+            PW_CUDA(cudaMemset(W.qflags, 0, sizeof(uint32_t) * n_chunks));  // tag 0 is never a call's
+            W.qflags_cap = n_chunks;
+        }
+        if (++W.qepoch == 0) {
+            PW_CUDA(cudaMemset(W.qflags, 0, sizeof(uint32_t) * W.qflags_cap));
+            W.qepoch = 1;
+        }
+        for (int64_t c = 0; c < n_chunks; c++) {
+            const int64_t lo = c * kChunk, rows = std::min<int64_t>(kChunk, q - lo);
+            PW_CUDA(cudaMemcpyAsync(dq + lo * d, queries + lo * d, sizeof(float) * rows * d, cudaMemcpyHostToDevice,
+                                    W.cs));
+            if (wv(W.cs, (CUdeviceptr)(W.qflags + c), W.qepoch, 0) != CUDA_SUCCESS)
+                return set_err(PW_ECUDA, "cuStreamWriteValue32 failed");
+        }
+        up = QUpload{W.qflags, kChunk, W.qepoch};
+        tl_upload = &up;
+    } else {
+        PW_CUDA(cudaMemcpyAsync(dq, queries, sizeof(float) * q * d, cudaMemcpyHostToDevice, st));
+    }
     PW_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
     rc = run_device_impl(W, shards, N, params, tuning, dq, q, mode, sid, sd, fid, fd, s32, s64,
                          (int32_t*)(b + o_ea), (int32_t*)(b + o_eb), err, st);
+    tl_upload = nullptr;
+    if (up.flags) PW_CUDA(cudaStreamSynchronize(W.cs));
     if (rc) return rc;
     int32_t herr = 0;
     PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
