@@ -1946,6 +1946,12 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
                 for (uint32_t spin = 0; ld_acquire_gpu_u32(f) != A.q_epoch; spin++) {
                     if (spin > (1u << 25)) {
                         atomicOr(A.err, 64);
+                        if (A.phase) {  // diagnostics: what was seen, where
+                            A.phase[0] = ld_acquire_gpu_u32(f);
+                            A.phase[1] = A.q_epoch;
+                            A.phase[2] = (unsigned long long)(f - A.qready);
+                            A.phase[3] = (unsigned long long)A.q_chunk;
+                        }
                         break;
                     }
                     __nanosleep(128);

@@ -1269,13 +1269,15 @@ int run_dataflow_local(RunWs& W, pw_shard* const* shards, int32_t N, const pw_pa
         W.inbox = nullptr;
         W.inbox_cap = 0;
         PW_CUDA(cudaMalloc(&W.inbox, words * sizeof(uint64_t)));
-        PW_CUDA(cudaMemset(W.inbox, 0, words * sizeof(uint64_t)));  // tag 0 is never a run's
+        // tag 0 is never a run's; ordered on st, which the ring streams wait
+        // for (a legacy-stream memset is not ordered with them)
+        PW_CUDA(cudaMemsetAsync(W.inbox, 0, words * sizeof(uint64_t), st));
         W.inbox_cap = words;
         W.epoch = 0;
     }
     if (++W.epoch == 0) {  // 2^32 runs: re-zero so no stale word can match
         PW_CUDA(cudaStreamSynchronize(st));
-        PW_CUDA(cudaMemset(W.inbox, 0, W.inbox_cap * sizeof(uint64_t)));
+        PW_CUDA(cudaMemsetAsync(W.inbox, 0, W.inbox_cap * sizeof(uint64_t), st));
         W.epoch = 1;
     }
     DevInfo* I;
@@ -1417,11 +1419,14 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
             W.qflags = nullptr;
             W.qflags_cap = 0;
             PW_CUDA(cudaMalloc(&W.qflags, sizeof(uint32_t) * n_chunks));
-            PW_CUDA(cudaMemset(W.qflags, 0, sizeof(uint32_t) * n_chunks));  // tag 0 is never a call's
+            // tag 0 is never a call's.  Ordered on the copy stream itself: a
+            // memset on the legacy stream is not ordered with a non-blocking
+            // stream and could land after this call's flag stores.
+            PW_CUDA(cudaMemsetAsync(W.qflags, 0, sizeof(uint32_t) * n_chunks, W.cs));
             W.qflags_cap = n_chunks;
         }
         if (++W.qepoch == 0) {
-            PW_CUDA(cudaMemset(W.qflags, 0, sizeof(uint32_t) * W.qflags_cap));
+            PW_CUDA(cudaMemsetAsync(W.qflags, 0, sizeof(uint32_t) * W.qflags_cap, W.cs));
             W.qepoch = 1;
         }
         for (int64_t c = 0; c < n_chunks; c++) {
@@ -1442,6 +1447,7 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     tl_upload = nullptr;
     if (up.flags) PW_CUDA(cudaStreamSynchronize(W.cs));
     if (rc) return rc;
+
     int32_t herr = 0;
     PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(shard_dists, sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
@@ -1451,6 +1457,14 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     PW_CUDA(cudaMemcpyAsync(stats_i64, s64, sizeof(int64_t) * q * N * 6, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(&herr, err, sizeof herr, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaStreamSynchronize(st));
+    if (up.flags && getenv("PW_UPLOAD_DEBUG")) {
+        unsigned long long ph[4];
+        PW_CUDA(cudaMemcpy(ph, shards[0]->phase, sizeof ph, cudaMemcpyDeviceToHost));
+        std::vector<uint32_t> fl(n_chunks);
+        PW_CUDA(cudaMemcpy(fl.data(), W.qflags, sizeof(uint32_t) * n_chunks, cudaMemcpyDeviceToHost));
+        fprintf(stderr, "pw_run upload: epoch %u chunks %lld flags[0] %u flags[last] %u | seen %llu want %llu at %llu chunk %llu\n",
+                W.qepoch, (long long)n_chunks, fl[0], fl[n_chunks - 1], ph[0], ph[1], ph[2], ph[3]);
+    }
     for (int s = 0; s < N; s++)
         if ((rc = check_err(shards[s]))) return rc;
     if (herr) return set_err(PW_EINVAL, "cannot reduce empty candidate lists");

@@ -353,3 +353,23 @@ def test_tma_gather4_rows_match_oracle(synth, d, arm, mode, flags):
     got = result_dict(runner(pw.Dataset(queries), None, None, params, contexts=ctxs, tuning={"flags": flags}))
     want = oracle_dict(oracle.run(queries, ctxs, params, mode))
     (assert_run_equal_lossy if flags & 2 else assert_run_equal)(got, want, f"tma d={d} arm={arm} {mode}")
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_pw_run_overlapped_upload(synth, pinned):
+    """pw_run uploads the queries in 512-row chunks on a copy stream while K1
+    runs, each chunk released by a flag K1 polls: 1537 queries (a partial
+    last chunk), page-locked or pageable, lossy (FAST kernel) and exact,
+    repeated calls (epoch tags) -- every result equal to the oracle."""
+    import torch
+    queries, ctxs = synth[96]
+    q = np.concatenate([queries, queries, queries])[:1537]
+    if pinned:
+        qp = torch.empty(q.shape, dtype=torch.float32, pin_memory=True).numpy()
+        qp[:] = q
+        q = qp
+    params = SearchParams(**SYNTH_ARMS[1])
+    want = oracle_dict(oracle.run(np.ascontiguousarray(q), ctxs, params, "pipelined"))
+    for tuning in (None, LOSSY, None):
+        got = result_dict(pw.run_pipelined(pw.Dataset(q), None, None, params, contexts=ctxs, tuning=tuning))
+        (assert_run_equal_lossy if tuning else assert_run_equal)(got, want, f"upload pinned={pinned} {tuning}")
