@@ -1841,27 +1841,13 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         S.c_ne += np;
         int nc = expand<D, VT, FAST>(A, S, G, C, parents, np, it, rng);
         PW_T(4);
-        if constexpr (FAST) {
-            // a table of next_pow2(2 nc) keys (load <= 1/2) is enough for this
-            // batch: clear only that much, and no position table (the ordered
-            // dedup and the exact visited path are not in this instance)
-            uint32_t hs = 64;
-            while (hs < 2u * (uint32_t)nc && hs < (uint32_t)A.BH) hs <<= 1;
-            uint4* k4 = reinterpret_cast<uint4*>(S.bhk);
-#pragma unroll 1
-            for (int i = lane; i < (int)(hs >> 2); i += 32) k4[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
-            __syncwarp();
-            nb = dedup_unordered(A, S, S.cand, nc, S.newl, hs - 1u);
-            S.c_tv += nb;
-        } else {
-            bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
-            if (nc <= C.cap && !C.log)
-                nb = dedup_unordered(A, S, S.cand, nc, S.newl, (uint32_t)A.BH - 1u);
-            else
-                nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
-            S.c_tv += nb;
-            bh_clear(A, S);
-        }
+        bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
+        if (FAST || (nc <= C.cap && !C.log))  // FAST: no buffer_cap, no visit log
+            nb = dedup_unordered(A, S, S.cand, nc, S.newl, (uint32_t)A.BH - 1u);
+        else
+            nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
+        S.c_tv += nb;
+        bh_clear(A, S);
         PW_T(5);
         n_new = visited_filter<(D > 0), FAST>(A, S, nb);
         PW_T(6);
