@@ -657,7 +657,9 @@ struct WarpState {
     int32_t fu;             // first queue position that may be unexpanded
     int32_t vcount;         // entries in the smem visited table
     bool ovf;               // visited set spilled to the global table
-    int64_t c_it, c_dc, c_tv, c_ne, c_dgs, c_ins;
+    // per-search counters, 32-bit (prepare() rejects budgets that could
+    // overflow them); StageStats accumulate them as int64
+    int32_t c_it, c_dc, c_tv, c_ne, c_dgs, c_ins;
 };
 
 __device__ __forceinline__ uint32_t bh_insert(const KArgs& A, WarpState& S, uint32_t id) {
@@ -1688,7 +1690,7 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
             __syncwarp();
         }
     }
-    S.c_dgs += (int64_t)np * (j - C.n_keep);
+    S.c_dgs += np * (j - C.n_keep);
     return np * nsel;
 }
 
@@ -1995,7 +1997,7 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
         __syncwarp();
 
         int32_t g_it = 0;
-        int64_t g_dc = 0, g_tv = 0, g_ne = 0;
+        int32_t g_dc = 0, g_tv = 0, g_ne = 0;  // ghost-stage counters (32-bit like the search's)
         int64_t n_logged = 0;
         const GraphDev& G = A.use_ghost_graph ? A.ghost : A.main;
 
@@ -2088,8 +2090,8 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
                     s32[1 * A.st_stride] = g_it;
                     s32[2 * A.st_stride] = S.qlen;
                     s32[3 * A.st_stride] = converged ? 1 : 0;
-                    s64[0 * A.st_stride] = S.c_dc + g_dc;
-                    s64[1 * A.st_stride] = S.c_tv + g_tv;
+                    s64[0 * A.st_stride] = (int64_t)S.c_dc + g_dc;
+                    s64[1 * A.st_stride] = (int64_t)S.c_tv + g_tv;
                     s64[2 * A.st_stride] = S.c_ins;
                     s64[3 * A.st_stride] = S.c_dgs;
                     s64[4 * A.st_stride] = S.c_ne;
@@ -2106,8 +2108,8 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
                 A.st32[1 * A.st_stride + task] += g_it;
                 A.st32[2 * A.st_stride + task] += S.qlen;
                 A.st32[3 * A.st_stride + task] = converged ? 1 : 0;
-                A.st64[0 * A.st_stride + task] += S.c_dc + g_dc;
-                A.st64[1 * A.st_stride + task] += S.c_tv + g_tv;
+                A.st64[0 * A.st_stride + task] += (int64_t)S.c_dc + g_dc;
+                A.st64[1 * A.st_stride + task] += (int64_t)S.c_tv + g_tv;
                 A.st64[2 * A.st_stride + task] += S.c_ins;
                 A.st64[3 * A.st_stride + task] += S.c_dgs;
                 A.st64[4 * A.st_stride + task] += S.c_ne;

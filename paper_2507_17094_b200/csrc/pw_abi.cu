@@ -575,6 +575,11 @@ int prepare(pw_shard* sh, const pw_params& p, const pw_tuning* tun, bool use_gho
                       offsetof(KArgs, gcfg) == offsetof(KArgs, cfg) + 2 * sizeof(SearchCfg),
                   "K1 indexes (&cfg)[0..2]");
     const int32_t Lq = std::max(p.l, lp.l);  // queue capacity (smem layout)
+    // K1 keeps per-search counters in 32 bits: every counter is bounded by
+    // want + max_iter * max(cap, r * j) (visits, scored rows, DGS skips)
+    for (const SearchCfg* c : {&A.cfg, &A.cfg_late})
+        if ((int64_t)c->want + (int64_t)c->max_iter * std::max<int64_t>(c->cap, (int64_t)c->r * G.j) >= (1ll << 31))
+            return set_err(PW_EINVAL, "max_iter too large for the device's per-search counters");
     A.ghost_on = ghost_on ? 1 : 0;
     A.seed_mode = p.seed_mode;
     A.use_ghost_graph = use_ghost_graph ? 1 : 0;
