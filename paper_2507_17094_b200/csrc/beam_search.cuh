@@ -300,6 +300,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #ifndef PW_DGS_LDG
 #define PW_DGS_LDG 0  // DGS parent rows into registers instead of the staging ring (A/B)
 #endif
+#ifndef PW_QREG_F32
+#define PW_QREG_F32 1  // float rows: this lane's query pairs held in registers while scoring
+#endif
 #ifndef PW_TMA_ROWS
 #define PW_TMA_ROWS 0
 #endif
@@ -978,7 +981,7 @@ __device__ int visited_filter(const KArgs& A, WarpState& S, int nb) {
 // completion on a per-half mbarrier, two halves in flight), and 16 rows are
 // reduced per warp pass in the compile-time pairwise order.  D == 0: generic
 // d (cp.async + runtime pairwise plan).
-template <int D, typename VT, int M, bool QI = false>
+template <int D, typename VT, int M, bool QI = false, bool QREG_OK = true>
 __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n, uint64_t thr) {
     const unsigned lane = lane_id();
     int ns = 0;  // survivors (key < thr, search.py:182-184) compacted into ckey as produced
@@ -1037,7 +1040,10 @@ __device__ int score_rows(const KArgs& A, WarpState& S, const GraphDev& G, int n
             cp_commit();
         };
         const unsigned v = lane >> 2, c = lane & 3u;
-        constexpr bool QREG = !QI && ((D <= 128 && D % 8 == 0) || sizeof(VT) == 1);
+        // float rows: query pairs in registers, except in the 96-register
+        // 20-warp build, where reading them from shared memory measured
+        // faster (ab_qreg_r02am.log)
+        constexpr bool QREG = !QI && ((PW_QREG_F32 && QREG_OK && D <= 128 && D % 8 == 0) || sizeof(VT) == 1);
         float2 qr[QREG ? D / 8 : 1];
         if constexpr (QREG) {
             const float2* q2 = reinterpret_cast<const float2*>(S.q);
@@ -1724,7 +1730,7 @@ static __device__ __noinline__ int64_t log_visits(int32_t* log, int64_t cap, con
 // One full search (search.py:269-335) over graph G.  Seeds (already in
 // S.cand[0..ns)) are deduplicated in order and capped at `want`; the
 // random fill draws Generator.choice(n, want) from rng.
-template <int D, typename VT, int M, bool FAST = false>
+template <int D, typename VT, int M, bool FAST = false, bool WIDE = false>
 __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const GraphDev& G, const SearchCfg& C,
                            int ns, bool fill_random, Pcg64& rng, int64_t task,
                            int64_t* n_logged) {
@@ -1822,7 +1828,7 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
                 ns = qmeta[1] ? score_rows<D, VT, M, true>(A, S, G, n_new, thr)
                               : score_rows<D, VT, M, false>(A, S, G, n_new, thr);
             } else {
-                ns = score_rows<D, VT, M>(A, S, G, n_new, thr);
+                ns = score_rows<D, VT, M, false, !WIDE>(A, S, G, n_new, thr);
             }
             PW_T(1);
             inserted = merge_queue(A, S, C, ns);
@@ -2036,7 +2042,8 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
                 rng = A.rng_io ? A.rng_io[task]
                                : pcg64_from_seed(derive_seed3(A.seed, 4, (uint64_t)tsk[0], (uint64_t)tsk[1]));
             }
-            converged = run_search<D, VT, M, FAST>(A, S, gph ? A.ghost : G, (&A.cfg)[gph ? 2 : (tsk[1] > 0 ? 1 : 0)],
+            converged = run_search<D, VT, M, FAST, (MAXT > PW_MAX_THREADS)>(A, S, gph ? A.ghost : G,
+                                                                         (&A.cfg)[gph ? 2 : (tsk[1] > 0 ? 1 : 0)],
                                              ns, fill_random, rng, task, &n_logged);
             if (gph) {
                 if (lane == 0) S.cand[0] = A.ghost.gid[(uint32_t)S.qk_cur()[0]];
