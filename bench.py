@@ -327,10 +327,12 @@ def run_ours(args, cfg):
         return eng.run(queries, params, mode, timer=timer)
 
     def search_stream(params, mode, steps, timer=None):
-        """`steps` back-to-back batches: the dataflow ring enqueues them with
-        no host synchronisation in between (double-buffered slots, device-side
-        landed/done flags); the single-GPU engine returns each batch."""
-        if use_df:
+        """`steps` back-to-back batches, enqueued with no host synchronisation
+        in between: the dataflow ring through double-buffered slots and
+        device-side landed/done flags, one rank through stream order (each
+        batch's final ids copied to page-locked host memory); the stage ring
+        returns each batch."""
+        if use_df or world == 1:
             for _ in range(steps):
                 eng.submit(queries, params, mode, timer=timer)
             eng.sync()

@@ -41,6 +41,8 @@ int set_err(int code, const std::string& msg) {
 
 int words_per_vector(int d) { return (d + 31) / 32; }
 int pw_fill_inf(float* p, int64_t n, cudaStream_t st);
+int pw_init_run(int32_t* ids, float* dists, int64_t n, int32_t* s32, int64_t n32, int64_t* s64, int64_t n64,
+                cudaStream_t st);
 
 int32_t keep_count(int32_t j, double discard) {  // direction.py:72-76
     int32_t v = (int32_t)((1.0 - discard) * (double)j + 0.5);
@@ -1234,6 +1236,10 @@ struct RunWs {
     uint32_t* qflags = nullptr;
     size_t qflags_cap = 0;
     uint32_t qepoch = 0;
+    // page-locked landing slots of pw_run's error flags (K2's, then one per
+    // shard), read with the results instead of one synchronous copy each
+    int32_t* hflags = nullptr;
+    bool k2_loaded = false;
 };
 RunWs g_ws[64];
 
@@ -1311,10 +1317,8 @@ int run_device_impl(RunWs& W, pw_shard* const* shards, int32_t N, const pw_param
     int rc = validate_params(*params);
     if (rc) return rc;
     const int64_t k = params->k;
-    PW_CUDA(cudaMemsetAsync(shard_ids, 0xFF, sizeof(int32_t) * q * N * k, st));  // -1 padding
-    if ((rc = pw_fill_inf(shard_dists, q * N * k, st))) return rc;               // +inf padding
-    PW_CUDA(cudaMemsetAsync(stats_i32, 0, sizeof(int32_t) * 4 * q * N, st));
-    PW_CUDA(cudaMemsetAsync(stats_i64, 0, sizeof(int64_t) * 6 * q * N, st));
+    if ((rc = pw_init_run(shard_ids, shard_dists, q * N * k, stats_i32, 4 * q * N, stats_i64, 6 * q * N, st)))
+        return rc;
     if (mode == PW_MODE_BASELINE) {
         for (int s = 0; s < N; s++) {  // pipeline.py:288-297
             rc = pw_search_stage(shards[s], params, tuning, queries, 0, q, s, nullptr, nullptr,
@@ -1411,36 +1415,57 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     int32_t* err = (int32_t*)(b + o_err);
     // Query upload overlapped with K1: chunks of kChunk rows on a copy stream,
     // each followed by a stream-ordered flag store (cuStreamWriteValue32) that
-    // the kernel polls before reading a row of that chunk.  Without the driver
-    // entry point: one copy ahead of the kernel on the same stream.
+    // the kernel polls before reading a row of that chunk.  With one shard,
+    // chunk 0 is enqueued before the kernel and the rest after its launch, so
+    // the copy API calls do not delay K1's start (nothing between that launch
+    // and those copies may block the host on the kernel: one stage launch and
+    // an asynchronous K2, its module loaded beforehand).  With several shards
+    // the launches may grow workspaces (a cudaFree synchronises the device),
+    // so every chunk is enqueued first.  Without the driver entry point: one copy ahead of the
+    // kernel on the same stream.
     constexpr int32_t kChunk = 512;
     const int64_t n_chunks = (q + kChunk - 1) / kChunk;
     WriteValue32Fn wv = write_value32();
     QUpload up{};
+    auto upload_chunk = [&](int64_t c) -> int {
+        const int64_t lo = c * kChunk, rows = std::min<int64_t>(kChunk, q - lo);
+        PW_CUDA(cudaMemcpyAsync(dq + lo * d, queries + lo * d, sizeof(float) * rows * d, cudaMemcpyHostToDevice,
+                                W.cs));
+        if (wv(W.cs, (CUdeviceptr)(W.qflags + c), W.qepoch, 0) != CUDA_SUCCESS)
+            return set_err(PW_ECUDA, "cuStreamWriteValue32 failed");
+        return 0;
+    };
     if (wv && q > kChunk) {
         if (!W.cs) PW_CUDA(cudaStreamCreateWithFlags(&W.cs, cudaStreamNonBlocking));
+        bool zero = false;
         if (W.qflags_cap < (size_t)n_chunks) {
             if (W.qflags) cudaFree(W.qflags);
             W.qflags = nullptr;
             W.qflags_cap = 0;
             PW_CUDA(cudaMalloc(&W.qflags, sizeof(uint32_t) * n_chunks));
-            // tag 0 is never a call's.  Ordered on the copy stream itself: a
-            // memset on the legacy stream is not ordered with a non-blocking
-            // stream and could land after this call's flag stores.
-            PW_CUDA(cudaMemsetAsync(W.qflags, 0, sizeof(uint32_t) * n_chunks, W.cs));
             W.qflags_cap = n_chunks;
+            zero = true;
         }
         if (++W.qepoch == 0) {
-            PW_CUDA(cudaMemsetAsync(W.qflags, 0, sizeof(uint32_t) * W.qflags_cap, W.cs));
             W.qepoch = 1;
+            zero = true;
         }
-        for (int64_t c = 0; c < n_chunks; c++) {
-            const int64_t lo = c * kChunk, rows = std::min<int64_t>(kChunk, q - lo);
-            PW_CUDA(cudaMemcpyAsync(dq + lo * d, queries + lo * d, sizeof(float) * rows * d, cudaMemcpyHostToDevice,
-                                    W.cs));
-            if (wv(W.cs, (CUdeviceptr)(W.qflags + c), W.qepoch, 0) != CUDA_SUCCESS)
-                return set_err(PW_ECUDA, "cuStreamWriteValue32 failed");
+        if (zero) {
+            // tag 0 is never a call's.  Complete before the kernel can poll: it
+            // runs on another stream, and fresh memory may hold any value.
+            PW_CUDA(cudaMemsetAsync(W.qflags, 0, sizeof(uint32_t) * W.qflags_cap, W.cs));
+            PW_CUDA(cudaStreamSynchronize(W.cs));
         }
+        if (N == 1 && !W.k2_loaded) {
+            // with lazy module loading (the CUDA 12 default) K2's first launch
+            // would load its module while K1 waits for the chunks enqueued
+            // after it, and the load waits for K1: load it now
+            cudaFuncAttributes fa;
+            PW_CUDA(cudaFuncGetAttributes(&fa, reduce_topk_kernel));
+            W.k2_loaded = true;
+        }
+        for (int64_t c = 0; c < (N == 1 ? 1 : n_chunks); c++)
+            if ((rc = upload_chunk(c))) return rc;
         up = QUpload{W.qflags, kChunk, W.qepoch};
         tl_upload = &up;
     } else {
@@ -1450,17 +1475,28 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     rc = run_device_impl(W, shards, N, params, tuning, dq, q, mode, sid, sd, fid, fd, s32, s64,
                          (int32_t*)(b + o_ea), (int32_t*)(b + o_eb), err, st);
     tl_upload = nullptr;
+    if (up.flags) {
+        // the remaining chunks, also when the launch failed part-way: a K1
+        // already running waits for them
+        for (int64_t c = N == 1 ? 1 : n_chunks; c < n_chunks; c++) {
+            const int rc2 = upload_chunk(c);
+            if (rc2 && !rc) rc = rc2;
+        }
+    }
+    if (!W.hflags) PW_CUDA(cudaMallocHost(&W.hflags, sizeof(int32_t) * (1 + 64)));
+    int32_t* hf = W.hflags;
     if (up.flags) PW_CUDA(cudaStreamSynchronize(W.cs));
     if (rc) return rc;
-
-    int32_t herr = 0;
     PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(shard_dists, sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(final_ids, fid, sizeof(int32_t) * q * k, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(final_dists, fd, sizeof(float) * q * k, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(stats_i32, s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
     PW_CUDA(cudaMemcpyAsync(stats_i64, s64, sizeof(int64_t) * q * N * 6, cudaMemcpyDeviceToHost, st));
-    PW_CUDA(cudaMemcpyAsync(&herr, err, sizeof herr, cudaMemcpyDeviceToHost, st));
+    PW_CUDA(cudaMemcpyAsync(hf, err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    for (int s = 0; s < N && s < 64; s++)
+        PW_CUDA(cudaMemcpyAsync(hf + 1 + s, shards[s]->counter + 1, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                st));
     PW_CUDA(cudaStreamSynchronize(st));
     if (up.flags && getenv("PW_UPLOAD_DEBUG")) {
         unsigned long long ph[4];
@@ -1471,7 +1507,8 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
                 W.qepoch, (long long)n_chunks, fl[0], fl[n_chunks - 1], ph[0], ph[1], ph[2], ph[3]);
     }
     for (int s = 0; s < N; s++)
-        if ((rc = check_err(shards[s]))) return rc;
+        if ((s >= 64 || hf[1 + s]) && (rc = check_err(shards[s]))) return rc;
+    const int32_t herr = hf[0];
     if (herr) return set_err(PW_EINVAL, "cannot reduce empty candidate lists");
     // comm accounting (pipeline.py:340-341): 4 B per forwarded entry
     std::memset(comm, 0, sizeof(int64_t) * N * N);
@@ -1636,6 +1673,30 @@ __global__ void fill_kernel(float* p, int64_t n, float v) {
 int pw_fill_inf(float* p, int64_t n, cudaStream_t st) {
     if (n <= 0) return 0;
     fill_kernel<<<(int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, st>>>(p, n, INFINITY);
+    g_launches++;
+    PW_CUDA(cudaGetLastError());
+    return 0;
+}
+
+// A run's output padding (-1 ids, +inf distances) and zeroed stats in one
+// launch instead of three memsets and a fill.
+__global__ void init_run_kernel(int32_t* ids, float* dists, int64_t n, int32_t* s32, int64_t n32, int64_t* s64,
+                                int64_t n64) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int64_t i = i0; i < n; i += stride) {
+        ids[i] = -1;
+        dists[i] = INFINITY;
+    }
+    for (int64_t i = i0; i < n32; i += stride) s32[i] = 0;
+    for (int64_t i = i0; i < n64; i += stride) s64[i] = 0;
+}
+
+int pw_init_run(int32_t* ids, float* dists, int64_t n, int32_t* s32, int64_t n32, int64_t* s64, int64_t n64,
+                cudaStream_t st) {
+    const int64_t m = std::max(n, std::max(n32, n64));
+    if (m <= 0) return 0;
+    init_run_kernel<<<(int)std::min<int64_t>(1024, (m + 255) / 256), 256, 0, st>>>(ids, dists, n, s32, n32, s64, n64);
     g_launches++;
     PW_CUDA(cudaGetLastError());
     return 0;

@@ -117,6 +117,33 @@ class RingSearch:
                 validate_inter(shard, sizes[(rank + 1) % world])
 
     # ---------------------------------------------------------------- device path
+    def submit(self, queries, params, mode: str, timer: list | None = None) -> None:
+        """One rank: enqueue a batch without host synchronisation; its final
+        ids land in a page-locked host buffer (`host_ids` after `sync`).
+        Consecutive batches reuse the device buffers in stream order, so the
+        host prepares batch b+1 while batch b runs.  N > 1 pipelines through
+        DataflowRing.submit."""
+        import torch
+
+        from . import device as dv
+
+        if self.world != 1:
+            raise ValueError("RingSearch.submit is the one-rank path; use DataflowRing for N > 1")
+        R = self.run_buf
+        dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning, stream=self.stream, timer=timer)
+        if getattr(self, "host_ids", None) is None or tuple(self.host_ids.shape) != tuple(R.final_ids.shape):
+            self.host_ids = torch.empty(tuple(R.final_ids.shape), dtype=torch.int32, pin_memory=True)
+        with torch.cuda.stream(self.stream):
+            self.host_ids.copy_(R.final_ids, non_blocking=True)
+
+    def sync(self) -> None:
+        """Wait for the submitted batches; raise on a device-side error."""
+        from . import device as dv
+
+        self.stream.synchronize()
+        self.run_buf.check()
+        dv.check_shard(self.shard)
+
     def run(self, queries, params, mode: str, timer: list | None = None) -> np.ndarray | None:
         """Search all queries; returns final ids (Q, k) numpy on rank 0."""
         import torch
@@ -227,8 +254,11 @@ class RingSearch:
                 self._host_out_key = key
             out = dict(self._host_out)
             handles = (C.c_void_p * 1)(self.shard.handle.value)
-            p = _abi.params_struct(params)
-            t = _abi.tuning_struct(self.tuning)
+            cached = getattr(self, "_host_structs", None)
+            if cached is None or cached[0] != params:
+                # ctypes structs built once per parameter set, not per call
+                cached = self._host_structs = (params, _abi.params_struct(params), _abi.tuning_struct(self.tuning))
+            p, t = cached[1], cached[2]
             _abi.check(lib.pw_run(handles, 1, C.byref(p), C.byref(t), queries_host.ctypes.data, q,
                                   _abi.MODE["pipelined"], out["shard_ids"].ctypes.data,
                                   out["shard_dists"].ctypes.data, out["final_ids"].ctypes.data,

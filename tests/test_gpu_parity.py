@@ -373,3 +373,32 @@ def test_pw_run_overlapped_upload(synth, pinned):
     for tuning in (None, LOSSY, None):
         got = result_dict(pw.run_pipelined(pw.Dataset(q), None, None, params, contexts=ctxs, tuning=tuning))
         (assert_run_equal_lossy if tuning else assert_run_equal)(got, want, f"upload pinned={pinned} {tuning}")
+
+
+@pytest.fixture(scope="module")
+def one_shard():
+    from index_util import clustered, make_contexts
+    x = clustered(24000 + 2600, 96, 512, 0.08, seed=7)
+    return np.ascontiguousarray(x[24000:]), make_contexts(x[:24000], 1, 32, seed=7)
+
+
+@pytest.mark.parametrize("mode", ["baseline", "pipelined"])
+def test_pw_run_one_shard_upload_after_launch(one_shard, mode):
+    """One shard and more than one 512-row chunk: pw_run enqueues chunk 0,
+    launches K1, then enqueues the other chunks while K1 runs (K2's module
+    loaded before the launch).  2600 queries (a partial last chunk), exact
+    and lossy, repeated calls (epoch tags) and a smaller batch in between --
+    ids, distances and every counter equal to the oracle."""
+    import torch
+    queries, ctxs = one_shard
+    qp = torch.empty(queries.shape, dtype=torch.float32, pin_memory=True).numpy()
+    qp[:] = queries
+    runner = pw.run_sharded_baseline if mode == "baseline" else pw.run_pipelined
+    params = SearchParams(**SYNTH_ARMS[1])
+    want = oracle_dict(oracle.run(queries, ctxs, params, mode))
+    want_small = oracle_dict(oracle.run(queries[:1100], ctxs, params, mode))
+    for tuning in (None, LOSSY, None, LOSSY):
+        got = result_dict(runner(pw.Dataset(qp), None, None, params, contexts=ctxs, tuning=tuning))
+        (assert_run_equal_lossy if tuning else assert_run_equal)(got, want, f"one shard {mode} {tuning}")
+        got = result_dict(runner(pw.Dataset(qp[:1100]), None, None, params, contexts=ctxs, tuning=tuning))
+        (assert_run_equal_lossy if tuning else assert_run_equal)(got, want_small, f"one shard small {mode} {tuning}")
