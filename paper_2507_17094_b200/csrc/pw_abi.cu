@@ -1239,7 +1239,6 @@ struct RunWs {
     // page-locked landing slots of pw_run's error flags (K2's, then one per
     // shard), read with the results instead of one synchronous copy each
     int32_t* hflags = nullptr;
-    bool k2_loaded = false;
 };
 RunWs g_ws[64];
 
@@ -1415,14 +1414,12 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     int32_t* err = (int32_t*)(b + o_err);
     // Query upload overlapped with K1: chunks of kChunk rows on a copy stream,
     // each followed by a stream-ordered flag store (cuStreamWriteValue32) that
-    // the kernel polls before reading a row of that chunk.  With one shard,
-    // chunk 0 is enqueued before the kernel and the rest after its launch, so
-    // the copy API calls do not delay K1's start (nothing between that launch
-    // and those copies may block the host on the kernel: one stage launch and
-    // an asynchronous K2, its module loaded beforehand).  With several shards
-    // the launches may grow workspaces (a cudaFree synchronises the device),
-    // so every chunk is enqueued first.  Without the driver entry point: one copy ahead of the
-    // kernel on the same stream.
+    // the kernel polls before reading a row of that chunk.  Every chunk is
+    // enqueued before the kernel's launch: a launch that blocks until the
+    // kernel ends (a profiler's serialised replay, CUDA_LAUNCH_BLOCKING,
+    // a synchronising call between launch and copies) would otherwise leave
+    // K1 waiting for copies not yet issued.  Without the driver entry point:
+    // one copy ahead of the kernel on the same stream.
     constexpr int32_t kChunk = 512;
     const int64_t n_chunks = (q + kChunk - 1) / kChunk;
     WriteValue32Fn wv = write_value32();
@@ -1456,15 +1453,7 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
             PW_CUDA(cudaMemsetAsync(W.qflags, 0, sizeof(uint32_t) * W.qflags_cap, W.cs));
             PW_CUDA(cudaStreamSynchronize(W.cs));
         }
-        if (N == 1 && !W.k2_loaded) {
-            // with lazy module loading (the CUDA 12 default) K2's first launch
-            // would load its module while K1 waits for the chunks enqueued
-            // after it, and the load waits for K1: load it now
-            cudaFuncAttributes fa;
-            PW_CUDA(cudaFuncGetAttributes(&fa, reduce_topk_kernel));
-            W.k2_loaded = true;
-        }
-        for (int64_t c = 0; c < (N == 1 ? 1 : n_chunks); c++)
+        for (int64_t c = 0; c < n_chunks; c++)
             if ((rc = upload_chunk(c))) return rc;
         up = QUpload{W.qflags, kChunk, W.qepoch};
         tl_upload = &up;
@@ -1475,14 +1464,6 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     rc = run_device_impl(W, shards, N, params, tuning, dq, q, mode, sid, sd, fid, fd, s32, s64,
                          (int32_t*)(b + o_ea), (int32_t*)(b + o_eb), err, st);
     tl_upload = nullptr;
-    if (up.flags) {
-        // the remaining chunks, also when the launch failed part-way: a K1
-        // already running waits for them
-        for (int64_t c = N == 1 ? 1 : n_chunks; c < n_chunks; c++) {
-            const int rc2 = upload_chunk(c);
-            if (rc2 && !rc) rc = rc2;
-        }
-    }
     if (!W.hflags) PW_CUDA(cudaMallocHost(&W.hflags, sizeof(int32_t) * (1 + 64)));
     int32_t* hf = W.hflags;
     if (up.flags) PW_CUDA(cudaStreamSynchronize(W.cs));

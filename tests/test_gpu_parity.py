@@ -6,6 +6,8 @@
   not cover (d = 96 / 128 / 200 / 960, 2-4 shards, thousands of queries).
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -383,12 +385,11 @@ def one_shard():
 
 
 @pytest.mark.parametrize("mode", ["baseline", "pipelined"])
-def test_pw_run_one_shard_upload_after_launch(one_shard, mode):
-    """One shard and more than one 512-row chunk: pw_run enqueues chunk 0,
-    launches K1, then enqueues the other chunks while K1 runs (K2's module
-    loaded before the launch).  2600 queries (a partial last chunk), exact
-    and lossy, repeated calls (epoch tags) and a smaller batch in between --
-    ids, distances and every counter equal to the oracle."""
+def test_pw_run_one_shard_chunked_upload(one_shard, mode):
+    """One shard and more than one 512-row upload chunk (the bench's e2e
+    shape): 2600 queries (a partial last chunk), exact and lossy, repeated
+    calls (epoch tags) and a smaller batch in between -- ids, distances and
+    every counter equal to the oracle."""
     import torch
     queries, ctxs = one_shard
     qp = torch.empty(queries.shape, dtype=torch.float32, pin_memory=True).numpy()
@@ -402,3 +403,28 @@ def test_pw_run_one_shard_upload_after_launch(one_shard, mode):
         (assert_run_equal_lossy if tuning else assert_run_equal)(got, want, f"one shard {mode} {tuning}")
         got = result_dict(runner(pw.Dataset(qp[:1100]), None, None, params, contexts=ctxs, tuning=tuning))
         (assert_run_equal_lossy if tuning else assert_run_equal)(got, want_small, f"one shard small {mode} {tuning}")
+
+
+def test_pw_run_upload_with_blocking_launches(tmp_path):
+    """CUDA_LAUNCH_BLOCKING=1 (as under a profiler's serialised replay: the
+    launch returns only when K1 ends): the chunked upload must be fully
+    enqueued before K1 is launched, or K1 waits for copies never issued."""
+    import os
+    import subprocess
+    import sys
+    script = tmp_path / "blocking.py"
+    script.write_text(
+        "import sys\n"
+        f"sys.path[:0] = [{str(Path(__file__).parent)!r}, {str(Path(__file__).parent.parent)!r}]\n"
+        "import numpy as np\n"
+        "import paper_2507_17094_b200 as pw\n"
+        "from index_util import clustered, make_contexts\n"
+        "from paper_2507_17094_b200.search import SearchParams\n"
+        "x = clustered(6000 + 1300, 32, 64, 0.08, seed=3)\n"
+        "ctxs = make_contexts(x[:6000], 1, 16, seed=3)\n"
+        "p = SearchParams(k=10, l=32, m=32, r=4, max_iter=16, seed=1)\n"
+        "r = pw.run_pipelined(pw.Dataset(np.ascontiguousarray(x[6000:])), None, None, p, contexts=ctxs)\n"
+        "print('ok', r.final_ids.shape)\n")
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "ok (1300, 10)" in out.stdout, out.stderr[-2000:]
