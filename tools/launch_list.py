@@ -7,7 +7,7 @@ import csv
 import sys
 from collections import defaultdict
 
-OURS = ("pw::", "knn::", "reduce_topk", "gather_rows", "fill_kernel", "l2_rows", "crc32c", "l2_pairs")
+OURS = ("pw::", "knn::", "reduce_topk", "gather_rows", "fill_kernel", "init_run_kernel", "l2_rows", "crc32c", "l2_pairs")
 
 path, cmd = sys.argv[1], (sys.argv[2] if len(sys.argv) > 2 else "")
 rows = []
