@@ -689,6 +689,9 @@ __device__ __forceinline__ bool bh_contains(const KArgs& A, const WarpState& S, 
     return false;
 }
 
+// KEYS_ONLY: only the key half (dedup_unordered's table; the position half
+// is read by dedup_ordered and the exact global visited path alone)
+template <bool KEYS_ONLY = false>
 __device__ __forceinline__ void bh_clear(const KArgs& A, WarpState& S) {
     uint4* k4 = reinterpret_cast<uint4*>(S.bhk);
     uint4* p4 = reinterpret_cast<uint4*>(S.bhp);
@@ -697,7 +700,7 @@ __device__ __forceinline__ void bh_clear(const KArgs& A, WarpState& S) {
 #pragma unroll 1
     for (int i = lane_id(); i < (A.BH >> 2); i += 32) {
         k4[i] = e;
-        p4[i] = m;
+        if (!KEYS_ONLY) p4[i] = m;
     }
     __syncwarp();
 }
@@ -1849,13 +1852,21 @@ __device__ __forceinline__ bool run_search(const KArgs& A, WarpState& S, const G
         S.c_ne += np;
         int nc = expand<D, VT, FAST>(A, S, G, C, parents, np, it, rng);
         PW_T(4);
-        bh_clear(A, S);  // the hash shares the staging ring, which now holds rows
-        if (FAST || (nc <= C.cap && !C.log))  // FAST: no buffer_cap, no visit log
+        // the hash shares the staging ring, which now holds rows.  FAST: the
+        // unordered dedup reads keys only, and the lossy visited cache does
+        // not use the hash (the next search's first clear is a full one)
+        if (FAST) {
+            bh_clear<true>(A, S);
             nb = dedup_unordered(A, S, S.cand, nc, S.newl, (uint32_t)A.BH - 1u);
-        else
-            nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
+        } else {
+            bh_clear(A, S);
+            if (nc <= C.cap && !C.log)
+                nb = dedup_unordered(A, S, S.cand, nc, S.newl, (uint32_t)A.BH - 1u);
+            else
+                nb = dedup_ordered(A, S, S.cand, nc, C.cap, S.newl, &nuniq);
+        }
         S.c_tv += nb;
-        bh_clear(A, S);
+        if (!FAST) bh_clear(A, S);
         PW_T(5);
         n_new = visited_filter<(D > 0), FAST>(A, S, nb);
         PW_T(6);
