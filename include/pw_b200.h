@@ -166,7 +166,12 @@ int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q
  * layer).  HOST buffers in and out: queries (q, d); shard_ids/dists (q, N, k);
  * final_ids/dists (q, k); stats_i32 (N, 4, q) / stats_i64 (N, 6, q) as in
  * pw_search_stage;
- * comm (N, N) int64 bytes per (stage, sending shard). */
+ * comm (N, N) int64 bytes per (stage, sending shard).
+ * Result block: when the six output buffers are one allocation laid out as
+ * shard_ids | shard_dists | final_ids | final_dists | stats_i32 | stats_i64,
+ * each starting at the previous one's start + its size rounded up to 256
+ * bytes, the results arrive in one copy instead of six (any other layout
+ * works too). */
 int pw_run(pw_shard* const* shards, int32_t n_shards, const pw_params* params,
            const pw_tuning* tuning, const float* queries, int64_t q, int32_t mode,
            int32_t* shard_ids, float* shard_dists, int32_t* final_ids, float* final_dists,

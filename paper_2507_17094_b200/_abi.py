@@ -186,3 +186,34 @@ def launch_config(shard_handle, params, tuning=None) -> dict:
     check(lib.pw_launch_config(shard_handle, C.byref(p), C.byref(t), out))
     return dict(warps_per_sm=out[0], smem_per_warp=out[1], visited_slots=out[2], stage_rows=out[3],
                 specialised_d=out[4], blocks=out[5])
+
+
+def result_block(q: int, n: int, k: int, pinned: bool = False) -> dict:
+    """pw_run's six output arrays as views into one allocation in the result
+    block layout of include/pw_b200.h (shard_ids | shard_dists | final_ids |
+    final_dists | stats_i32 | stats_i64, each at the previous start + its
+    size rounded up to 256 bytes), so pw_run copies them in one transfer.
+    `pinned`: page-locked (torch) memory, DMA straight into it."""
+    import numpy as np
+
+    specs = (("shard_ids", (q, n, k), np.int32), ("shard_dists", (q, n, k), np.float32),
+             ("final_ids", (q, k), np.int32), ("final_dists", (q, k), np.float32),
+             ("s32", (n, 4, q), np.int32), ("s64", (n, 6, q), np.int64))
+    offs, total = [], 0
+    for _, shape, dt in specs:
+        offs.append(total)
+        nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
+        total += (nbytes + 255) // 256 * 256
+    if pinned:
+        import torch
+
+        raw = torch.empty(total + 256, dtype=torch.uint8, pin_memory=True).numpy()
+    else:
+        raw = np.empty(total + 256, np.uint8)
+    base = (-raw.ctypes.data) % 256  # 256-byte aligned start (not required, but tidy)
+    out = {}
+    for (name, shape, dt), o in zip(specs, offs):
+        nbytes = int(np.prod(shape)) * np.dtype(dt).itemsize
+        out[name] = raw[base + o:base + o + nbytes].view(dt).reshape(shape)
+    out["_raw"] = raw  # keeps the allocation alive with the views
+    return out

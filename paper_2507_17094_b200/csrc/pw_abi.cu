@@ -1468,12 +1468,25 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     int32_t* hf = W.hflags;
     if (up.flags) PW_CUDA(cudaStreamSynchronize(W.cs));
     if (rc) return rc;
-    PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
-    PW_CUDA(cudaMemcpyAsync(shard_dists, sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
-    PW_CUDA(cudaMemcpyAsync(final_ids, fid, sizeof(int32_t) * q * k, cudaMemcpyDeviceToHost, st));
-    PW_CUDA(cudaMemcpyAsync(final_dists, fd, sizeof(float) * q * k, cudaMemcpyDeviceToHost, st));
-    PW_CUDA(cudaMemcpyAsync(stats_i32, s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
-    PW_CUDA(cudaMemcpyAsync(stats_i64, s64, sizeof(int64_t) * q * N * 6, cudaMemcpyDeviceToHost, st));
+    // the results: one copy when the host buffers form the documented result
+    // block (the device workspace holds them in that layout), else six
+    char* h0 = reinterpret_cast<char*>(shard_ids);
+    const bool block = reinterpret_cast<char*>(shard_dists) == h0 + (o_sd - o_sid) &&
+                       reinterpret_cast<char*>(final_ids) == h0 + (o_fid - o_sid) &&
+                       reinterpret_cast<char*>(final_dists) == h0 + (o_fd - o_sid) &&
+                       reinterpret_cast<char*>(stats_i32) == h0 + (o_s32 - o_sid) &&
+                       reinterpret_cast<char*>(stats_i64) == h0 + (o_s64 - o_sid);
+    if (block) {
+        PW_CUDA(cudaMemcpyAsync(h0, b + o_sid, (o_s64 - o_sid) + sizeof(int64_t) * q * N * 6,
+                                cudaMemcpyDeviceToHost, st));
+    } else {
+        PW_CUDA(cudaMemcpyAsync(shard_ids, sid, sizeof(int32_t) * q * N * k, cudaMemcpyDeviceToHost, st));
+        PW_CUDA(cudaMemcpyAsync(shard_dists, sd, sizeof(float) * q * N * k, cudaMemcpyDeviceToHost, st));
+        PW_CUDA(cudaMemcpyAsync(final_ids, fid, sizeof(int32_t) * q * k, cudaMemcpyDeviceToHost, st));
+        PW_CUDA(cudaMemcpyAsync(final_dists, fd, sizeof(float) * q * k, cudaMemcpyDeviceToHost, st));
+        PW_CUDA(cudaMemcpyAsync(stats_i32, s32, sizeof(int32_t) * q * N * 4, cudaMemcpyDeviceToHost, st));
+        PW_CUDA(cudaMemcpyAsync(stats_i64, s64, sizeof(int64_t) * q * N * 6, cudaMemcpyDeviceToHost, st));
+    }
     PW_CUDA(cudaMemcpyAsync(hf, err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     for (int s = 0; s < N && s < 64; s++)
         PW_CUDA(cudaMemcpyAsync(hf + 1 + s, shards[s]->counter + 1, sizeof(int32_t), cudaMemcpyDeviceToHost,

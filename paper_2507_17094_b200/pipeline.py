@@ -193,12 +193,11 @@ def _run(mode: str, queries, index, dataset, params: SearchParams, contexts, tun
     handles = (C.c_void_p * n)(*[d.handle.value for d in devs])
     p = _abi.params_struct(params)
     t = _abi.tuning_struct(tuning)
-    shard_ids = np.empty((q, n, k), np.int32)
-    shard_dists = np.empty((q, n, k), np.float32)
-    final_ids = np.empty((q, k), np.int32)
-    final_dists = np.empty((q, k), np.float32)
-    s32 = np.empty((n, 4, q), np.int32)
-    s64 = np.empty((n, 6, q), np.int64)
+    # one result block: pw_run copies the six arrays back in one transfer
+    res = _abi.result_block(q, n, k)
+    shard_ids, shard_dists = res["shard_ids"], res["shard_dists"]
+    final_ids, final_dists = res["final_ids"], res["final_dists"]
+    s32, s64 = res["s32"], res["s64"]
     comm = np.empty((n, n), np.int64)
     _abi.check(lib.pw_run(handles, n, C.byref(p), C.byref(t), qdata.ctypes.data, q,
                           _abi.MODE[mode], shard_ids.ctypes.data, shard_dists.ctypes.data,

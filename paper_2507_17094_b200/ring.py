@@ -237,20 +237,13 @@ class RingSearch:
             lib = _abi.load()
             q = queries_host.shape[0]
             k = int(params.k)
-            # page-locked result buffers, reused across calls (DMA straight
-            # into them; pageable memory would go through a driver bounce copy)
+            # one page-locked result block, reused across calls: pw_run copies
+            # it back in one transfer (pageable memory would go through a
+            # driver bounce copy)
             key = (q, k)
             if getattr(self, "_host_out_key", None) != key:
-                import torch
-
-                def pinned(shape, dt):
-                    return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
-
-                self._host_out = dict(
-                    shard_ids=pinned((q, 1, k), torch.int32), shard_dists=pinned((q, 1, k), torch.float32),
-                    final_ids=pinned((q, k), torch.int32), final_dists=pinned((q, k), torch.float32),
-                    s32=pinned((1, 4, q), torch.int32), s64=pinned((1, 6, q), torch.int64),
-                    comm=np.empty((1, 1), np.int64))
+                self._host_out = _abi.result_block(q, 1, k, pinned=True)
+                self._host_out["comm"] = np.empty((1, 1), np.int64)
                 self._host_out_key = key
             out = dict(self._host_out)
             handles = (C.c_void_p * 1)(self.shard.handle.value)
@@ -264,7 +257,7 @@ class RingSearch:
                                   out["shard_dists"].ctypes.data, out["final_ids"].ctypes.data,
                                   out["final_dists"].ctypes.data, out["s32"].ctypes.data,
                                   out["s64"].ctypes.data, out["comm"].ctypes.data))
-            out["bytes_out"] = sum(v.nbytes for key, v in out.items() if key != "comm")
+            out["bytes_out"] = sum(v.nbytes for key, v in out.items() if key not in ("comm", "_raw"))
             return out
         import torch
 

@@ -102,3 +102,23 @@ def test_no_odd_uniform_memory_descriptors():
     # descriptors (`idesc[..]`, `gdesc[..]`) are other operand kinds
     odd = sorted(set(re.findall(r"(?<![a-z])desc\[UR\d*[13579]\]", sass)))
     assert not odd, odd
+
+
+def test_result_block_layout():
+    """_abi.result_block follows include/pw_b200.h's result block: the six
+    arrays in order, each at the previous start + its size rounded up to 256
+    bytes, with the documented shapes and dtypes."""
+    import numpy as np
+
+    from paper_2507_17094_b200 import _abi
+    for q, n, k in ((10000, 1, 10), (1537, 3, 16), (1, 2, 100)):
+        b = _abi.result_block(q, n, k)
+        names = ("shard_ids", "shard_dists", "final_ids", "final_dists", "s32", "s64")
+        shapes = ((q, n, k), (q, n, k), (q, k), (q, k), (n, 4, q), (n, 6, q))
+        dts = (np.int32, np.float32, np.int32, np.float32, np.int32, np.int64)
+        addr = b["shard_ids"].ctypes.data
+        for name, shape, dt in zip(names, shapes, dts):
+            a = b[name]
+            assert a.shape == shape and a.dtype == dt and a.flags.c_contiguous, name
+            assert a.ctypes.data == addr, name
+            addr += (a.nbytes + 255) // 256 * 256

@@ -428,3 +428,32 @@ def test_pw_run_upload_with_blocking_launches(tmp_path):
     env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
     out = subprocess.run([sys.executable, str(script)], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ok (1300, 10)" in out.stdout, out.stderr[-2000:]
+
+
+def test_pw_run_result_block_and_separate_buffers(one_shard, synth):
+    """pw_run's results are the same whether the six host buffers form the
+    documented result block (one copy back) or are separate allocations (six
+    copies): byte-equal arrays, one shard and a pipelined 2-shard run."""
+    import ctypes as C
+
+    from paper_2507_17094_b200 import _abi
+    from paper_2507_17094_b200.pipeline import device_shard
+    lib = _abi.load()
+    params = SearchParams(**SYNTH_ARMS[1])
+    for queries, ctxs in (one_shard, synth[96]):
+        devs = [device_shard(c) for c in ctxs]
+        n, q, k = len(devs), queries.shape[0], params.k
+        handles = (C.c_void_p * n)(*[d.handle.value for d in devs])
+        p, t = _abi.params_struct(params), _abi.tuning_struct(None)
+        blk = _abi.result_block(q, n, k)
+        sep = dict(shard_ids=np.empty((q, n, k), np.int32), shard_dists=np.empty((q, n, k), np.float32),
+                   final_ids=np.empty((q, k), np.int32), final_dists=np.empty((q, k), np.float32),
+                   s32=np.empty((n, 4, q), np.int32), s64=np.empty((n, 6, q), np.int64))
+        for out in (blk, sep):
+            comm = np.empty((n, n), np.int64)
+            _abi.check(lib.pw_run(handles, n, C.byref(p), C.byref(t), queries.ctypes.data, q, 1,
+                                  out["shard_ids"].ctypes.data, out["shard_dists"].ctypes.data,
+                                  out["final_ids"].ctypes.data, out["final_dists"].ctypes.data,
+                                  out["s32"].ctypes.data, out["s64"].ctypes.data, comm.ctypes.data))
+        for key in sep:
+            assert np.array_equal(blk[key].view(np.uint8), sep[key].view(np.uint8)), (n, key)
