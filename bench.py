@@ -81,10 +81,16 @@ CONFIGS = {
     "c4": dict(workload="GIST-shaped 1M x 960 f32, 1K queries, k=10, degree-32 graph", n=1_000_000,
                d=960, nq=1_000, k=10, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05,
                rho=0.01, j_g=16, probe=48, builder="exact"),
+    # exact graph through K4 with the query block streamed per K atom (d = 200)
     "c5s": dict(workload="Text2Image-shaped 12.5M x 200 f32 inner product (one of C5's 8 shards of "
                          "100M), 10K queries, k=100, degree-32 graph", n=12_500_000, d=200, nq=10_000,
                 k=100, j=32, gen="latent", m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01,
-                j_g=16, probe=192, refine=1, metric="ip"),
+                j_g=16, probe=192, metric="ip", builder="exact"),
+    # round-1 / round-2 C5s: approximate IVF graph
+    "c5sivf": dict(workload="Text2Image-shaped 12.5M x 200 f32 inner product (one of C5's 8 shards of "
+                            "100M), 10K queries, k=100, degree-32 graph (IVF approximate graph)",
+                   n=12_500_000, d=200, nq=10_000, k=100, j=32, gen="latent", m=16, n_clusters=1, spread=1.0,
+                   noise=0.05, rho=0.01, j_g=16, probe=192, refine=1, metric="ip"),
     "tiny": dict(workload="smoke 20K x 96", n=20_000, d=96, nq=1_000, k=10, j=32, gen="latent",
                  m=16, n_clusters=1, spread=1.0, noise=0.05, rho=0.01, j_g=16, probe=8),
 }

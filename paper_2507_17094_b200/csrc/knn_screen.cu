@@ -41,6 +41,9 @@ struct Args {
     float* out_vals;           // (nq, kc)
     uint32_t o_b, o_bar, o_lv, o_li, o_tmem, o_nb, o_scr;  // shared-memory offsets
     int32_t debug;             // A/B probes: 1 skip the compare loop, 2 no norm loads
+    int32_t stream_a;          // 1: the query block does not fit beside the ring (d > 128 with
+                               // 64-candidate lists): ring stages hold one K atom of the query
+                               // block AND of the column tile, the query atoms re-read (L2) per tile
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -173,44 +176,87 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (elect_one()) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_q) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tm_x) : "memory");
-            mbar_expect_tx(a_full, (uint32_t)(BM * KA * ATOM));
-            for (int a = 0; a < KA; a++) tma_load_2d(sa + (size_t)a * BM * ATOM, &tm_q, 32 * a, (int32_t)row0, a_full);
-            for (int64_t t = 0; t < ntiles; t++) {
-                const int s = (int)(t % ST);
-                const uint32_t ph = (uint32_t)((t / ST) & 1);
-                mbar_wait(empty + s, ph ^ 1u);
-                mbar_expect_tx(full + s, b_stage_bytes);
-                unsigned char* dst = sb + (size_t)s * b_stage_bytes;
+            if (!A.stream_a) {
+                mbar_expect_tx(a_full, (uint32_t)(BM * KA * ATOM));
                 for (int a = 0; a < KA; a++)
-                    tma_load_2d(dst + (size_t)a * BN * ATOM, &tm_x, 32 * a, (int32_t)(t * BN), full + s);
+                    tma_load_2d(sa + (size_t)a * BM * ATOM, &tm_q, 32 * a, (int32_t)row0, a_full);
+                for (int64_t t = 0; t < ntiles; t++) {
+                    const int s = (int)(t % ST);
+                    const uint32_t ph = (uint32_t)((t / ST) & 1);
+                    mbar_wait(empty + s, ph ^ 1u);
+                    mbar_expect_tx(full + s, b_stage_bytes);
+                    unsigned char* dst = sb + (size_t)s * b_stage_bytes;
+                    for (int a = 0; a < KA; a++)
+                        tma_load_2d(dst + (size_t)a * BN * ATOM, &tm_x, 32 * a, (int32_t)(t * BN), full + s);
+                }
+            } else {
+                // one stage per (tile, K atom): the query atom, then the column atom
+                const uint32_t st_bytes = (uint32_t)((BM + BN) * ATOM);
+                int64_t i = 0;
+                for (int64_t t = 0; t < ntiles; t++)
+                    for (int a = 0; a < KA; a++, i++) {
+                        const int s = (int)(i % ST);
+                        const uint32_t ph = (uint32_t)((i / ST) & 1);
+                        mbar_wait(empty + s, ph ^ 1u);
+                        mbar_expect_tx(full + s, st_bytes);
+                        unsigned char* dst = sb + (size_t)s * st_bytes;
+                        tma_load_2d(dst, &tm_q, 32 * a, (int32_t)row0, full + s);
+                        tma_load_2d(dst + (size_t)BM * ATOM, &tm_x, 32 * a, (int32_t)(t * BN), full + s);
+                    }
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (one thread)
         const uint32_t idesc = idesc_tf32(BM, BN);
         const uint32_t sa_u = smem_u32(sa), sb_u = smem_u32(sb);
-        mbar_wait(a_full, 0);
-        for (int64_t t = 0; t < ntiles; t++) {
-            const int s = (int)(t % ST);
-            const uint32_t ph = (uint32_t)((t / ST) & 1);
-            const int buf = (int)(t & 1);
-            const uint32_t aph = (uint32_t)((t >> 1) & 1);
-            mbar_wait(acc_empty + buf, aph ^ 1u);  // epilogue drained this accumulator
-            mbar_wait(full + s, ph);               // tile landed
-            tc_fence_after();
-            if (elect_one()) {
-                const uint32_t d_tmem = tmem + (uint32_t)(buf * BN);
-                const uint32_t b0 = sb_u + (uint32_t)s * b_stage_bytes;
-                for (int a = 0; a < KA; a++)
-                    for (int kk = 0; kk < 4; kk++) {  // K = 8 tf32 = 32 bytes per instruction
-                        const uint64_t da = sw128_desc(sa_u + (uint32_t)(a * BM * ATOM + kk * 32));
-                        const uint64_t db = sw128_desc(b0 + (uint32_t)(a * BN * ATOM + kk * 32));
-                        mma_tf32(d_tmem, da, db, idesc, (a | kk) ? 1u : 0u);
-                    }
-                mma_commit(empty + s);        // ring slot free once these MMAs have read it
-                mma_commit(acc_full + buf);   // accumulator ready for the epilogue
+        if (!A.stream_a) {
+            mbar_wait(a_full, 0);
+            for (int64_t t = 0; t < ntiles; t++) {
+                const int s = (int)(t % ST);
+                const uint32_t ph = (uint32_t)((t / ST) & 1);
+                const int buf = (int)(t & 1);
+                const uint32_t aph = (uint32_t)((t >> 1) & 1);
+                mbar_wait(acc_empty + buf, aph ^ 1u);  // epilogue drained this accumulator
+                mbar_wait(full + s, ph);               // tile landed
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t d_tmem = tmem + (uint32_t)(buf * BN);
+                    const uint32_t b0 = sb_u + (uint32_t)s * b_stage_bytes;
+                    for (int a = 0; a < KA; a++)
+                        for (int kk = 0; kk < 4; kk++) {  // K = 8 tf32 = 32 bytes per instruction
+                            const uint64_t da = sw128_desc(sa_u + (uint32_t)(a * BM * ATOM + kk * 32));
+                            const uint64_t db = sw128_desc(b0 + (uint32_t)(a * BN * ATOM + kk * 32));
+                            mma_tf32(d_tmem, da, db, idesc, (a | kk) ? 1u : 0u);
+                        }
+                    mma_commit(empty + s);        // ring slot free once these MMAs have read it
+                    mma_commit(acc_full + buf);   // accumulator ready for the epilogue
+                }
+                __syncwarp();
             }
-            __syncwarp();
+        } else {
+            const uint32_t st_bytes = (uint32_t)((BM + BN) * ATOM);
+            int64_t i = 0;
+            for (int64_t t = 0; t < ntiles; t++) {
+                const int buf = (int)(t & 1);
+                const uint32_t aph = (uint32_t)((t >> 1) & 1);
+                const uint32_t d_tmem = tmem + (uint32_t)(buf * BN);
+                mbar_wait(acc_empty + buf, aph ^ 1u);
+                for (int a = 0; a < KA; a++, i++) {
+                    const int s = (int)(i % ST);
+                    const uint32_t ph = (uint32_t)((i / ST) & 1);
+                    mbar_wait(full + s, ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t a0 = sb_u + (uint32_t)s * st_bytes, b0 = a0 + (uint32_t)(BM * ATOM);
+                        for (int kk = 0; kk < 4; kk++)
+                            mma_tf32(d_tmem, sw128_desc(a0 + (uint32_t)(kk * 32)), sw128_desc(b0 + (uint32_t)(kk * 32)),
+                                     idesc, (a | kk) ? 1u : 0u);
+                        mma_commit(empty + s);
+                        if (a == KA - 1) mma_commit(acc_full + buf);
+                    }
+                    __syncwarp();
+                }
+            }
         }
     } else {
         // ---------------- epilogue: warp w reads TMEM lanes 32 * (w % 4) ..
@@ -378,15 +424,27 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const size_t a_bytes = (size_t)BM * ka * ATOM;
     const size_t lists = (size_t)kc * BM * 8;
-    int bn = 0, st = 0;
+    const size_t fixed = 1024 + lists + 2048 + 32 * BM * 4;
+    int bn = 0, st = 0, stream_a = 0;
     for (int cand_bn : {128, 64, 32})
         for (int cand_st : {4, 3, 2}) {
-            const size_t need = a_bytes + (size_t)cand_st * cand_bn * ka * ATOM + 1024 + lists + 2048 + 32 * BM * 4;
+            const size_t need = a_bytes + (size_t)cand_st * cand_bn * ka * ATOM + fixed;
             if (!bn && need <= (size_t)optin) {
                 bn = cand_bn;
                 st = cand_st;
             }
         }
+    if (!bn || (bn < 128 && ka > 4)) {
+        // large d: stream the query block per K atom beside the column atoms
+        // (1-atom stages, so the ring is deep enough to cover the TMA latency)
+        bn = 0;
+        for (int cand_st : {8, 6, 5, 4, 3})
+            if (!bn && (size_t)cand_st * (BM + 128) * ATOM + fixed <= (size_t)optin) {
+                bn = 128;
+                st = cand_st;
+                stream_a = 1;
+            }
+    }
     if (!bn) {
         snprintf(msg, 256, "knn screen: d=%d needs more shared memory than the device has", d);
         return -1;
@@ -404,9 +462,10 @@ extern "C" int pw_knn_screen_impl(const float* q, int64_t nq, const float* x, in
     A.out_ids = out_ids;
     A.out_vals = out_vals;
     A.debug = debug;
-    size_t off = a_bytes;
+    A.stream_a = stream_a;
+    size_t off = stream_a ? 0 : a_bytes;
     A.o_b = (uint32_t)off;
-    off += (size_t)st * bn * ka * ATOM;
+    off += stream_a ? (size_t)st * (BM + bn) * ATOM : (size_t)st * bn * ka * ATOM;
     A.o_bar = (uint32_t)off;
     off += 8 * (1 + 2 * st + 4);
     A.o_tmem = (uint32_t)off;

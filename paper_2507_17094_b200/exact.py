@@ -161,8 +161,7 @@ def exact_topk(base: torch.Tensor, queries: torch.Tensor, k: int, exclude_self: 
     redone by the FP32 screen), "auto" (tc for large problems)."""
     nq, n, d = queries.shape[0], base.shape[0], base.shape[1]
     kc = k + pad + (1 if exclude_self else 0)
-    use_tc = screen == "tc" or (screen == "auto" and nq * n >= TC_MIN_PAIRS and kc <= 64 and d % 4 == 0
-                                and d <= 128)  # K4 keeps the 128-row query block resident
+    use_tc = screen == "tc" or (screen == "auto" and nq * n >= TC_MIN_PAIRS and kc <= 64 and d % 4 == 0)
     if not use_tc:
         cand = _screen(base, queries, kc)
         return _rescore_rank(base, queries, cand, k, exclude_self)
