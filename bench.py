@@ -295,7 +295,10 @@ def run_ours(args, cfg):
     dev = torch.device("cuda", local)
     # NCCL over NVLink in production; PW_DIST_BACKEND=gloo lets several ranks
     # share one GPU to exercise the multi-rank flow where only one GPU exists
-    backend = os.environ.get("PW_DIST_BACKEND", "nccl")
+    # (NCCL refuses two ranks on one device, so more ranks than GPUs default
+    # to gloo for the plumbing; the data path is the same CUDA IPC ring)
+    backend = os.environ.get("PW_DIST_BACKEND",
+                             "nccl" if world <= max(1, torch.cuda.device_count()) else "gloo")
     if world > 1:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
