@@ -138,9 +138,10 @@ struct KArgs {
     // task waits for its entry, which shard g-1 stores straight into this
     // shard's inbox (P2P over NVLink between GPUs) when its stage s-1 search
     // ends -- no stage barriers, no host round trips (pipeline.py:327-347).
-    // Overlapped query upload (pw_run): query rows arrive in chunks of
-    // q_chunk rows on a copy stream, each chunk's flag set to q_epoch after it
-    // lands; a task polls its chunk's flag before reading its row.
+    // Overlapped query upload (pw_run): query rows arrive in geometrically
+    // growing chunks (chunk c: rows [q_chunk (2^c - 1), q_chunk (2^(c+1) - 1)))
+    // on a copy stream, each chunk's flag set to q_epoch after it lands; a
+    // task polls its chunk's flag before reading its row.
     const uint32_t* qready;  // or null (queries already resident)
     int32_t q_chunk;
     uint32_t q_epoch;
@@ -1960,7 +1961,9 @@ __global__ void __launch_bounds__(MAXT, 1) beam_search_kernel(const __grid_const
         if (A.qready) {
             // overlapped upload: wait (bounded) for this row's chunk to land
             if (lane == 0) {
-                const uint32_t* f = A.qready + (A.df ? row : A.q0 + row) / A.q_chunk;
+                // chunk c holds rows [q_chunk (2^c - 1), q_chunk (2^(c+1) - 1))
+                const int64_t qr = A.df ? row : A.q0 + row;
+                const uint32_t* f = A.qready + (31 - __clz((int)(qr / A.q_chunk) + 1));
                 for (uint32_t spin = 0; ld_acquire_gpu_u32(f) != A.q_epoch; spin++) {
                     if (spin > (1u << 25)) {
                         atomicOr(A.err, 64);

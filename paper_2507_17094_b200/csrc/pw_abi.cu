@@ -1420,12 +1420,19 @@ int pw_run(pw_shard* const* shards, int32_t N, const pw_params* params, const pw
     // a synchronising call between launch and copies) would otherwise leave
     // K1 waiting for copies not yet issued.  Without the driver entry point:
     // one copy ahead of the kernel on the same stream.
-    constexpr int32_t kChunk = 512;
-    const int64_t n_chunks = (q + kChunk - 1) / kChunk;
+    // Chunks grow geometrically (kChunk, 2 kChunk, 4 kChunk, ... rows: chunk c
+    // starts at row kChunk (2^c - 1)), so the first rows land within a few
+    // microseconds while the whole upload takes few API calls before the
+    // launch (6 for 10K queries instead of 20 fixed 512-row chunks: each
+    // copy + flag pair costs the host ~5 us, all of it before K1 starts).
+    constexpr int32_t kChunk = 256;
+    auto chunk_lo = [](int64_t c) { return (int64_t)kChunk * ((1ll << c) - 1); };
+    int64_t n_chunks = 0;
+    while (chunk_lo(n_chunks) < q) n_chunks++;
     WriteValue32Fn wv = write_value32();
     QUpload up{};
     auto upload_chunk = [&](int64_t c) -> int {
-        const int64_t lo = c * kChunk, rows = std::min<int64_t>(kChunk, q - lo);
+        const int64_t lo = chunk_lo(c), rows = std::min<int64_t>((int64_t)kChunk << c, q - lo);
         PW_CUDA(cudaMemcpyAsync(dq + lo * d, queries + lo * d, sizeof(float) * rows * d, cudaMemcpyHostToDevice,
                                 W.cs));
         if (wv(W.cs, (CUdeviceptr)(W.qflags + c), W.qepoch, 0) != CUDA_SUCCESS)

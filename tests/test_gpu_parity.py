@@ -359,9 +359,9 @@ def test_tma_gather4_rows_match_oracle(synth, d, arm, mode, flags):
 
 @pytest.mark.parametrize("pinned", [False, True])
 def test_pw_run_overlapped_upload(synth, pinned):
-    """pw_run uploads the queries in 512-row chunks on a copy stream while K1
-    runs, each chunk released by a flag K1 polls: 1537 queries (a partial
-    last chunk), page-locked or pageable, lossy (FAST kernel) and exact,
+    """pw_run uploads the queries in growing chunks (256, 512, 1024, ... rows)
+    on a copy stream while K1 runs, each chunk released by a flag K1 polls:
+    1537 queries (a partial last chunk), page-locked or pageable, lossy (FAST kernel) and exact,
     repeated calls (epoch tags) -- every result equal to the oracle."""
     import torch
     queries, ctxs = synth[96]
@@ -386,8 +386,8 @@ def one_shard():
 
 @pytest.mark.parametrize("mode", ["baseline", "pipelined"])
 def test_pw_run_one_shard_chunked_upload(one_shard, mode):
-    """One shard and more than one 512-row upload chunk (the bench's e2e
-    shape): 2600 queries (a partial last chunk), exact and lossy, repeated
+    """One shard and several upload chunks (the bench's e2e shape): 2600
+    queries (a partial fourth chunk), exact and lossy, repeated
     calls (epoch tags) and a smaller batch in between -- ids, distances and
     every counter equal to the oracle."""
     import torch
