@@ -404,8 +404,7 @@ def run_ours(args, cfg):
     def timed(kind, steps, warmup, with_timer=False):
         p = arm_params(kind, ops[kind]["l"], k, metric, ops[kind]["discard"], ops[kind]["ghost_iter"])
         mode = ops[kind]["mode"]
-        for _ in range(warmup):
-            search(p, mode)
+        search_stream(p, mode, warmup)  # the timed path itself, warm
         launches0 = lib.pw_launch_count()
         timers = [] if with_timer else None
         if world > 1:

@@ -160,6 +160,13 @@ int pw_reduce_topk(const int32_t* shard_ids, const float* shard_dists, int64_t q
                    int32_t n_cand, int32_t k, int32_t* final_ids, float* final_dists,
                    int32_t* err_dev, void* stream);
 
+/* Output initialisation of a device-resident run (no reference counterpart:
+ * the reference allocates fresh arrays per call, pipeline.py:288-305): ids[n]
+ * = -1 and dists[n] = +inf (the shard-column padding), s32[n32] = 0 and
+ * s64[n64] = 0 (StageStats), in one launch on `stream`. */
+int pw_init_outputs(int32_t* ids, float* dists, int64_t n, int32_t* s32, int64_t n32,
+                    int64_t* s64, int64_t n64, void* stream);
+
 /* Replaces pipeline.py:270-305 run_sharded_baseline (mode 0) and
  * :308-350 run_pipelined (mode 1) for n_shards shards resident on the
  * current device (logical shards; the multi-GPU ring lives in the host

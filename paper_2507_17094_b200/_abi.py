@@ -73,6 +73,8 @@ EXPORTS = {
                                   C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_int64, C.c_void_p]),
+    "pw_init_outputs": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                                  C.c_int64, C.c_void_p]),
     "pw_reduce_topk": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "pw_run": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(Params), C.POINTER(Tuning), C.c_void_p,
@@ -107,7 +109,7 @@ EXPORTS = {
     "pw_crc32c_device": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
 }
 
-OPTIONAL = {"pw_shard_validate_inter", "pw_signal", "pw_wait", "pw_phase_cycles", "pw_launch_config", "pw_search_dataflow", "pw_shard_check", "pw_l2_pairs", "pw_knn_screen", "pw_gather_probe", "pw_dev_alloc", "pw_dev_free",
+OPTIONAL = {"pw_init_outputs", "pw_shard_validate_inter", "pw_signal", "pw_wait", "pw_phase_cycles", "pw_launch_config", "pw_search_dataflow", "pw_shard_check", "pw_l2_pairs", "pw_knn_screen", "pw_gather_probe", "pw_dev_alloc", "pw_dev_free",
             "pw_ipc_get", "pw_ipc_open", "pw_ipc_close"}
 _LIB = None
 

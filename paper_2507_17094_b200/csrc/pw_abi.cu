@@ -1703,3 +1703,10 @@ int pw_init_run(int32_t* ids, float* dists, int64_t n, int32_t* s32, int64_t n32
     return 0;
 }
 }  // namespace
+
+extern "C" int pw_init_outputs(int32_t* ids, float* dists, int64_t n, int32_t* s32, int64_t n32, int64_t* s64,
+                               int64_t n64, void* stream) {
+    if ((n > 0 && (!ids || !dists)) || (n32 > 0 && !s32) || (n64 > 0 && !s64))
+        return set_err(PW_EINVAL, "null argument");
+    return pw_init_run(ids, dists, n, s32, n32, s64, n64, (cudaStream_t)stream);
+}

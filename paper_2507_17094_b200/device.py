@@ -97,11 +97,12 @@ class DeviceRun:
         self.entries = [torch.zeros(q * 8, dtype=torch.int32, device=dev) for _ in range(2)]
         self.err = reduce_flag()
 
-    def reset(self):
-        self.shard_ids.fill_(-1)
-        self.shard_dists.fill_(float("inf"))
-        self.s32.zero_()
-        self.s64.zero_()
+    def reset(self, stream=None):
+        """Padding (-1 / +inf) and zeroed StageStats, one launch on `stream`."""
+        st = (stream or torch.cuda.current_stream(self.shard_ids.device)).cuda_stream
+        _abi.check(_abi.load().pw_init_outputs(self.shard_ids.data_ptr(), self.shard_dists.data_ptr(),
+                                               self.shard_ids.numel(), self.s32.data_ptr(), self.s32.numel(),
+                                               self.s64.data_ptr(), self.s64.numel(), C.c_void_p(st)))
 
     def check(self) -> None:
         """Read and clear the K2 flag (synchronises): the device-resident
@@ -154,13 +155,15 @@ def chunk_bounds(q: int, n: int) -> list[int]:
 
 
 def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: str, run: DeviceRun,
-              tuning=None, stream=None, timer: list | None = None) -> None:
+              tuning=None, stream=None, timer: list | None = None, reduce_after=None) -> None:
     """All shards on this device: baseline (shard s = stage s, all queries) or
     pipelined (chunk c stage s on shard (c+s)%N, entry forwarded in HBM).
     If `timer` is a list, (start, end) CUDA events bracket every search launch.
     `params` may be a list of N SearchParams, one per stage (per-stage
     budgets, SPEC.md "a per-stage budget vector is configurable"; an opt-in
-    extension -- the reference's run_pipelined uses one parameter set)."""
+    extension -- the reference's run_pipelined uses one parameter set).
+    `reduce_after`: a CUDA event the final reduce waits for (a reader of the
+    previous batch's final lists on another stream)."""
     n = len(shards)
     per_stage = list(params) if isinstance(params, (list, tuple)) else [params] * n
     if len(per_stage) != n or len({p.k for p in per_stage}) != 1:
@@ -178,8 +181,7 @@ def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: st
             e1.record(stream)
             timer.append((e0, e1))
 
-    with torch.cuda.stream(stream):
-        run.reset()
+    run.reset(stream)
     if mode == "baseline":
         for s in range(n):
             launch(shards[s], per_stage[s], queries, 0, q, s, run, s, s)
@@ -193,6 +195,8 @@ def run_local(shards: list[TensorShard], params, queries: torch.Tensor, mode: st
                        stage, entries_in=ein if stage > 0 else None,
                        forward_out=eout if stage < n - 1 else None)
             ein, eout = eout, ein
+    if reduce_after is not None:
+        stream.wait_event(reduce_after)
     reduce(run, stream)
 
 

@@ -107,6 +107,17 @@ class RingSearch:
         self.stream = torch.cuda.current_stream(self.dev)
         self._lib = None
         self.gloo = False
+        if world == 1:
+            # submit()'s final-id copies go to the host on a side stream, so
+            # batch b+1's K1 starts right after batch b's reduce; batch b+1's
+            # reduce waits for that copy before overwriting the lists.  Made
+            # here: the first stream from torch's pool and the page-locked
+            # buffer cost milliseconds once.
+            self._d2h = torch.cuda.Stream(self.dev)
+            self._ev_reduced = torch.cuda.Event()
+            self._ev_copied = torch.cuda.Event()
+            self._ev_copied.record(self._d2h)
+            self.host_ids = torch.empty((q, k), dtype=torch.int32, pin_memory=True)
         if world > 1:
             import torch.distributed as dist
 
@@ -117,6 +128,8 @@ class RingSearch:
                 validate_inter(shard, sizes[(rank + 1) % world])
 
     # ---------------------------------------------------------------- device path
+    side_d2h = True  # final-id copies on a side stream (A/B: False = in stream order)
+
     def submit(self, queries, params, mode: str, timer: list | None = None) -> None:
         """One rank: enqueue a batch without host synchronisation; its final
         ids land in a page-locked host buffer (`host_ids` after `sync`).
@@ -130,17 +143,30 @@ class RingSearch:
         if self.world != 1:
             raise ValueError("RingSearch.submit is the one-rank path; use DataflowRing for N > 1")
         R = self.run_buf
-        dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning, stream=self.stream, timer=timer)
+        if not self.side_d2h:
+            dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning, stream=self.stream, timer=timer)
+            if getattr(self, "host_ids", None) is None or tuple(self.host_ids.shape) != tuple(R.final_ids.shape):
+                self.host_ids = torch.empty(tuple(R.final_ids.shape), dtype=torch.int32, pin_memory=True)
+            with torch.cuda.stream(self.stream):
+                self.host_ids.copy_(R.final_ids, non_blocking=True)
+            return
+        dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning, stream=self.stream, timer=timer,
+                     reduce_after=self._ev_copied)
         if getattr(self, "host_ids", None) is None or tuple(self.host_ids.shape) != tuple(R.final_ids.shape):
             self.host_ids = torch.empty(tuple(R.final_ids.shape), dtype=torch.int32, pin_memory=True)
-        with torch.cuda.stream(self.stream):
+        self._ev_reduced.record(self.stream)
+        self._d2h.wait_event(self._ev_reduced)
+        with torch.cuda.stream(self._d2h):
             self.host_ids.copy_(R.final_ids, non_blocking=True)
+        self._ev_copied.record(self._d2h)
 
     def sync(self) -> None:
         """Wait for the submitted batches; raise on a device-side error."""
         from . import device as dv
 
         self.stream.synchronize()
+        if getattr(self, "_d2h", None) is not None:
+            self._d2h.synchronize()
         self.run_buf.check()
         dv.check_shard(self.shard)
 
