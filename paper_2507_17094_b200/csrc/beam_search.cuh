@@ -304,6 +304,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #ifndef PW_QREG_F32
 #define PW_QREG_F32 1  // float rows: this lane's query pairs held in registers while scoring
 #endif
+#ifndef PW_DGS_QREG
+#define PW_DGS_QREG 1  // DGS: the query elements in registers across the parent loop (0.7% on C2 K1, ab_qr8_s17.log)
+#endif
+#ifndef PW_DGS_PUNROLL
+#define PW_DGS_PUNROLL 1  // DGS parent loop unrolled by 2 (A/B)
+#endif
 #ifndef PW_TMA_ROWS
 #define PW_TMA_ROWS 0
 #endif
@@ -1604,10 +1610,20 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                         });
             if (WC > 0 && j <= 32) {
                 const unsigned valid = __ballot_sync(0xffffffffu, (int)lane < j);
+#if PW_DGS_QREG
+                // this lane's query elements for the direction bits, loaded once
+                // per expansion instead of once per parent
+                float qv[WC > 0 ? WC : 1];
+#pragma unroll
+                for (int w = 0; w < WC; w++) qv[w] = 32 * w + (int)lane < d ? S.q[32 * w + lane] : 0.f;
+#endif
                 // per parent: query direction bits pack(q >= x_parent) as W
                 // ballots (direction.py:53-59), matching count per slot
                 // (lane = slot, :62-69), one warp bitonic sort on (count desc,
                 // slot asc) == stable argsort(-counts) (:79-87)
+#if PW_DGS_PUNROLL == 2
+#pragma unroll 2
+#endif
                 for (int pi = 0; pi < gp; pi++) {
                     uint32_t qb[WC > 0 ? WC : 1];
 #pragma unroll
@@ -1616,7 +1632,11 @@ __device__ int expand(const KArgs& A, WarpState& S, const GraphDev& G, const Sea
                             qb[w] = qbits[pi * WC + w];
                         } else {
                             const int t = 32 * w + (int)lane;
+#if PW_DGS_QREG
+                            const bool bit = t < d && qv[w] >= to_f(prow[(size_t)pi * A.pstride + t]);
+#else
                             const bool bit = t < d && S.q[t] >= to_f(prow[(size_t)pi * A.pstride + t]);
+#endif
                             qb[w] = __ballot_sync(0xffffffffu, bit);
                         }
                     }
