@@ -267,7 +267,9 @@ def ground_truth(W: dict, k: int, metric: str = "l2") -> np.ndarray:
 # (l=384); at discard 0.8: ghost_max_iter 16 3.98, 8 3.40, 4 3.04 (no ghost
 # stage at all: 2.72 -- an ablation, not the PathWeaver arm); m 32/64/128 and
 # r 6/10 no better than m=64, r=8.
-PW_GRID = tuple((dr, gi) for dr in (0.5, 0.7, 0.75, 0.8) for gi in (8, 4, 2, 1))
+# (0.85 discards pay off with more shards: 3.01x naive at 8 logical shards,
+# profiles/r02/logical_c2_hi_s22.jsonl)
+PW_GRID = tuple((dr, gi) for dr in (0.5, 0.7, 0.75, 0.8) for gi in (8, 4, 2, 1)) + ((0.85, 2), (0.85, 1))
 
 
 def arm_params(kind: str, l: int, k: int, metric: str = "l2", discard: float = 0.5, ghost_iter: int = 8):
