@@ -182,7 +182,7 @@ class RingSearch:
             raise ValueError("forward_count > 1 needs the dataflow ring (PW_RING=dataflow)")
         if self.world == 1:
             dv.run_local([self.shard], params, queries, mode, R, tuning=self.tuning,
-                         stream=self.stream, timer=timer)
+                         stream=self.stream, timer=timer, reduce_after=getattr(self, "_ev_copied", None))
             ids = R.final_ids.cpu().numpy()
             R.check()
             return ids

@@ -112,3 +112,46 @@ def test_concurrent_searches_on_one_shard_match_serial():
         for _ in range(3):
             assert list(ex.map(one, range(48))) == serial
     torch.cuda.synchronize()
+
+
+def test_init_outputs_one_launch():
+    """pw_init_outputs (DeviceRun.reset): padding ids -1, distances +inf,
+    StageStats zero, whatever the buffers held before."""
+    run = dv.DeviceRun(257, 3, 7, "cuda")
+    for t in (run.shard_ids, run.s32, run.s64):
+        t.fill_(12345)
+    run.shard_dists.fill_(0.5)
+    run.reset()
+    torch.cuda.synchronize()
+    assert bool((run.shard_ids == -1).all()) and bool(torch.isinf(run.shard_dists).all())
+    assert int(run.s32.abs().sum()) == 0 and int(run.s64.abs().sum()) == 0
+
+
+def test_submit_batches_equal_run():
+    """RingSearch.submit (the bench's device loop: final-id copies on a side
+    stream, the next batch's reduce ordered after the previous copy) returns
+    the same ids as the synchronous run, batch after batch, alternating
+    parameter sets."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).parent))
+    from df_util import tensor_shard
+    from paper_2507_17094_b200 import ring
+
+    z, base, queries, index, ctxs = load("small")
+    shard = tensor_shard(ctxs[0])
+    q = torch.from_numpy(np.ascontiguousarray(queries)).cuda()
+    eng = ring.RingSearch(shard, q.shape[0], 10, 0, 1, "cuda", tuning={"flags": 2})
+    pa = SearchParams(k=10, l=32, m=32, r=4, max_iter=24, seed=17)
+    pb = SearchParams(k=10, l=48, m=32, r=4, max_iter=24, seed=5, selection="direction", discard_ratio=0.5)
+    want = {id(p): eng.run(q, p, "baseline") for p in (pa, pb)}
+    for p in (pa, pb, pa, pb, pb):
+        eng.submit(q, p, "baseline")
+        eng.sync()
+        assert np.array_equal(eng.host_ids.numpy(), want[id(p)])
+    for _ in range(4):  # back to back without host synchronisation: the last batch's lists land
+        eng.submit(q, pa, "baseline")
+    eng.submit(q, pb, "baseline")
+    eng.sync()
+    assert np.array_equal(eng.host_ids.numpy(), want[id(pb)])
